@@ -1,0 +1,339 @@
+"""Benchmark: agent-updates/s of the fp64 mechanical-interaction step on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line on rank 0.  A "step" is one full reference step (engine.py:279-341):
+Z-order re-sort, grid rebuild, 27-box force sweep, adherence gate, capped
+displacement, apply -- on the device-resident population.
+
+* value    -- agent-updates/s over all ranks, inputs resident in HBM, CUDA
+              events on the context stream, max over ranks.
+* e2e      -- the same metric through the public drop-in API
+              (engine.step(pool, SimulationConfig(strategy=Gpu()))) with the
+              pool in pinned host memory: H2D of the pool + step + D2H of the
+              updated pool inside the timed region, every step.
+* roofline -- the dominant kernel (the force sweep) against MEASURED_PEAKS.json
+              hbm_gbs, algorithmic bytes 64 B/agent (fp64).
+* cpu_baseline -- the C oracle (restatement of the reference path, OpenMP on
+              all host cores) on rank 0, bounded sample of the same workload.
+
+``--impl reference`` times the reference CPU path (the oracle port, all host
+threads) on the same config and prints the same line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "agent-updates/s per mechanical step (fp64) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "agent-updates/s"
+B_ALG = {"fp64": 64, "fp32": 32}     # 5 scalars read + 3 written per agent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", help="c4 (default), c2, c1, c3_<density>")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--summation", default="stencil", choices=["uid", "stencil"])
+    ap.add_argument("--box-order", default="rowmajor", choices=["morton", "rowmajor"])
+    ap.add_argument("--sort-every", type=int, default=1)
+    ap.add_argument("--freeze", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def make_pool(name, precision, rank=0, world=1):
+    from paper_2105_00039_b200 import workloads
+    from paper_2105_00039_b200.pool import PrecisionMode
+    pm = PrecisionMode.FP64 if precision == "fp64" else PrecisionMode.FP32
+    if name == "c4":
+        return (workloads.c4(pm) if world == 1 else workloads.c5_shard(rank, world, pm)), \
+            "C4: 256^3 jittered lattice (spacing 8, diameter 10, jitter +-1), 16,777,216 agents" + \
+            ("" if world == 1 else " per rank (C5 slab %d of %d)" % (rank, world))
+    if name == "c2":
+        return workloads.c2(pm), "C2: 1M uniform random, ref-density 27"
+    if name == "c1":
+        return workloads.c1(pm), "C1: 32^3 lattice spacing 8"
+    if name.startswith("c3_"):
+        c = float(name[3:])
+        return workloads.c3(c, pm), "C3: 2M uniform random, %g colliding neighbours/agent" % c
+    raise SystemExit("unknown config %s" % name)
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = [v for v in sm if mx and v > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def profiled_traffic(config, precision):
+    """Per-launch DRAM bytes of the sweep from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get("%s_%s" % (config, precision))
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_port_run(pool, precision, steps, sort_every, freeze):
+    """The oracle (C restatement of the reference step) on all host threads;
+    returns (median seconds per step, threads)."""
+    import oracle
+    from paper_2105_00039_b200.mechanics import ForceParams
+    th = cpu_threads()
+    oracle.lib()
+    ts = []
+    for k in range(steps):
+        t0 = time.perf_counter()
+        oracle.step(pool, ForceParams(), sort=(sort_every > 0 and k % sort_every == 0),
+                    freeze=freeze, threads=th)
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts)), th
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def reduce_max(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    pool, desc = make_pool(args.config, args.precision)
+    n = pool.count
+    # bounded sample: the full workload while K+W full steps fit in ~3 min, else fewer steps
+    t_one, th = cpu_port_run(pool, args.precision, 1, args.sort_every, args.freeze)
+    k_total = args.steps + args.warmup
+    k_run = max(1, min(args.steps, int(180.0 / max(t_one, 1e-3)) - 1))
+    t_med, th = cpu_port_run(pool, args.precision, k_run, args.sort_every, args.freeze)
+    v = n / t_med
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": k_run, "warmup": 1, "ms_per_step": t_med * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": desc, "agents": n, "sort_every": args.sort_every,
+                       "freeze": args.freeze, "cpu_threads": th},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": "port",
+                             "sample": "%d full step(s) of the %d-agent workload (requested K+W=%d)"
+                                       % (k_run, n, k_total)},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    from paper_2105_00039_b200 import _native
+    from paper_2105_00039_b200 import engine as eng
+    from paper_2105_00039_b200.pool import PrecisionMode
+
+    torch.cuda.set_device(local)
+    pool, desc = make_pool(args.config, args.precision, rank, world)
+    n = pool.count
+    flags_for = lambda k: ((_native.CG_STEP_SORT if args.sort_every > 0 and k % args.sort_every == 0 else 0)
+                           | (_native.CG_STEP_FREEZE if args.freeze else 0))
+    ctx = _native.Context(local, pool.dtype)
+    ctx.set_option(_native.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[args.summation])
+    ctx.set_option(_native.CG_OPT_BOX_ORDER, {"morton": 0, "rowmajor": 1}[args.box_order])
+    ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence,
+               pool.uid)
+    params = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
+    for k in range(args.warmup):
+        ctx.step(params, None, 1 << 24, flags_for(k))
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
+    barrier(world)
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        ids = [ctx.step(params, None, 1 << 24, flags_for(args.warmup + k), wait=False)
+               for k in range(args.steps)]
+        ev1.record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    barrier(world)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = reduce_max(ms, world)
+    stats = [ctx.fetch_stats(i) for i in ids[-min(len(ids), 60):]]
+    t_force = float(np.mean([s.t_force_ms for s in stats]))
+    evals = float(np.mean([s.force_evals for s in stats]))
+    cands = float(np.mean([s.candidates for s in stats]))
+    value = n * world / (ms * 1e-3)
+    ctx.close()
+
+    # e2e: the public drop-in API with pinned host columns, H2D + step + D2H every step
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = _native.PinnedArray.copy_of
+        from paper_2105_00039_b200.pool import AgentPool
+        hp = AgentPool(position_x=pin(pool.position_x), position_y=pin(pool.position_y),
+                       position_z=pin(pool.position_z), diameter=pin(pool.diameter),
+                       adherence=pin(pool.adherence), uid=pin(pool.uid),
+                       displacement_x=pin(pool.displacement_x), displacement_y=pin(pool.displacement_y),
+                       displacement_z=pin(pool.displacement_z))
+        cfg = eng.SimulationConfig(strategy=eng.Gpu(device=local, summation=args.summation,
+                                                    box_order=args.box_order),
+                                   precision=PrecisionMode.FP64 if args.precision == "fp64" else PrecisionMode.FP32,
+                                   morton_sort_every=args.sort_every, freeze_displacement=args.freeze)
+        eng.step(hp, cfg, 0)                       # warm the context
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(args.e2e_steps):
+            eng.step(hp, cfg, k + 1)
+        torch.cuda.synchronize()
+        t_e2e = reduce_max((time.perf_counter() - t0) / args.e2e_steps, world)
+        es = np.dtype(pool.dtype).itemsize
+        e2e = {"value": n * world / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": n * (5 * es + 8), "d2h_bytes_per_step": n * (8 * es + 8),
+               "ms_per_step": t_e2e * 1e3, "api": "engine.step(pool, SimulationConfig(strategy=Gpu()))"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cp, _ = make_pool(args.config, args.precision)
+        t_med, th = cpu_port_run(cp, args.precision, args.cpu_steps, args.sort_every, args.freeze)
+        cpu = {"value": cp.count / t_med, "unit": UNIT, "cores": th, "kind": "port",
+               "sample": "%d full step(s) of the same %d-agent workload, median" % (args.cpu_steps, cp.count)}
+
+    if rank != 0:
+        return
+    peak, peak_src = measured_hbm_peak()
+    bal = B_ALG[args.precision]
+    achieved = n * bal / (t_force * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": desc, "agents_per_gpu": n, "sort_every": args.sort_every,
+                   "freeze": args.freeze, "summation": args.summation, "box_order": args.box_order,
+                   "l2": "inputs larger than L2 (%.0f MB of agent state per GPU)" % (n * (6 * np.dtype(pool.dtype).itemsize + 8) / 1e6),
+                   "parallelism": "single GPU" if world == 1 else "replicas x%d (no halo exchange)" % world},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.precision),
+                     "kernel": "sweep_kernel", "alg_bytes_per_agent": bal,
+                     "kernel_ms": t_force, "peak_source": peak_src},
+        "step_roofline_frac": n * bal / (ms * 1e-3) / 1e9 / peak,
+        "pair_interactions_per_s": evals * world / (ms * 1e-3),
+        "candidates_per_s": cands * world / (ms * 1e-3),
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

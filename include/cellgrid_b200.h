@@ -1,0 +1,132 @@
+/*
+ * cellgrid_b200.h -- C ABI of the B200 mechanical-interaction step.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types).  A context owns all
+ * device buffers of one agent population on one GPU; they persist across
+ * steps.  Host buffers are borrowed for the duration of a call.  Calls on one
+ * context must be serialised by the caller (reference SPEC.md:462: the engine
+ * is not shared across concurrent step calls).  Every entry point returns a
+ * CG_* status; cg_last_error() holds the message of the last failure.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/cellgrid/):
+ *   cg_step          engine.py:279-341  step(pool, config, step_index)
+ *                    (sort -> grid -> force -> apply, counters of StepStats)
+ *   cg_box_ids       kernels.py:107-129 box_ids_parallel(...)
+ *   cg_force_phase   kernels.py:302-333 force_phase_parallel(...) -> (evals, cands, ndeg)
+ *   cg_build_grid +  spatial.py:89-127  build_grid(...) -> UniformGrid (box_index, box_count)
+ *   cg_grid_export
+ *   cg_upload/download  the AgentPool SoA columns (pool.py:58-66) crossing the boundary
+ * Status codes map 1:1 onto the reference exception classes (see
+ * paper_2105_00039_b200/_native.py).
+ */
+#ifndef CELLGRID_B200_H
+#define CELLGRID_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CG_ABI_VERSION 1
+
+/* status codes */
+#define CG_OK 0
+#define CG_ERR_VALUE 1          /* ValueError (bad argument, empty pool, dtype) */
+#define CG_ERR_GRID_OVERFLOW 2  /* spatial.GridOverflowError (spatial.py:111-116) */
+#define CG_ERR_STENCIL 3        /* spatial.StencilTooSmallError (spatial.py:143-145) */
+#define CG_ERR_POOL_CAPACITY 4  /* pool.PoolCapacityError (pool.py:151-152) */
+#define CG_ERR_CUDA 5           /* CUDA runtime failure */
+#define CG_ERR_NO_DEVICE 6      /* no sm_100 device / bad ordinal */
+#define CG_ERR_STATE 7          /* call out of order (e.g. step before upload) */
+
+/* precision (PrecisionMode, pool.py:34-46) */
+#define CG_FP64 0
+#define CG_FP32 1
+
+/* cg_step flags */
+#define CG_STEP_SORT 1          /* Z-order re-sort due this step (engine.py:305-309) */
+#define CG_STEP_FREEZE 2        /* SimulationConfig.freeze_displacement (engine.py:324) */
+#define CG_STEP_RECORD 4        /* keep per-agent m / nk for cg_record_export */
+
+/* cg_set_option keys */
+#define CG_OPT_SUMMATION 1      /* 0 = uid order (bit-exact vs reference), 1 = stencil order */
+#define CG_OPT_BOX_ORDER 2      /* 0 = Morton (reference storage order), 1 = row-major */
+
+typedef struct cg_context cg_context;
+
+/* Per-step statistics: the StepStats fields (engine.py:134-151) the path owns. */
+typedef struct {
+    int64_t step_id;
+    int64_t agent_count;
+    int64_t force_evals;        /* ordered pairs with positive overlap */
+    int64_t candidates;         /* ordered stencil pairs examined */
+    int64_t degenerate_pairs;   /* coincident-centre pairs */
+    int64_t grid_dims[3];
+    int64_t grid_occupied_boxes;
+    int64_t grid_max_occupancy;
+    double box_length;
+    double origin[3];
+    float t_sort_ms, t_grid_ms, t_force_ms, t_total_ms;   /* CUDA-event times */
+} cg_step_stats;
+
+int cg_abi_version(void);
+int cg_device_count(int *count);
+
+int cg_create(int device, int precision, cg_context **out);
+void cg_destroy(cg_context *ctx);
+const char *cg_last_error(const cg_context *ctx);
+int cg_set_option(cg_context *ctx, int key, int value);
+/* Opaque cudaStream_t of the context (for event timing by the caller). */
+void *cg_stream(cg_context *ctx);
+
+/* Columns in the context precision; uid is uint64.  n may be 0. */
+int cg_upload(cg_context *ctx, int64_t n, const void *px, const void *py, const void *pz,
+              const void *diameter, const void *adherence, const uint64_t *uid);
+/* Any pointer may be NULL to skip that column.  Storage order is the device
+ * order, which equals the reference's after a Morton-sorted step. */
+int cg_download(cg_context *ctx, void *px, void *py, void *pz, void *diameter,
+                void *adherence, uint64_t *uid, void *dx, void *dy, void *dz);
+int64_t cg_count(const cg_context *ctx);
+/* Kernels launched by this context so far (evidence for bench gpu_launches). */
+int64_t cg_launch_count(const cg_context *ctx);
+/* Page-locked host memory for staging pool columns (NULL on failure). */
+void *cg_host_alloc(int64_t bytes);
+void cg_host_free(void *p);
+
+/* One mechanical step.  params = ForceParams (kappa, gamma, timestep,
+ * max_displacement, adherence_scale), mechanics.py:47-75.
+ * interaction_radius: NaN = None.  box_cap: spatial.DEFAULT_BOX_CAP (1<<24).
+ * If stats != NULL the call waits for the step and fills it; otherwise the
+ * step is only enqueued and cg_fetch_stats(step_id) collects it later. */
+int cg_step(cg_context *ctx, const double params[5], double interaction_radius,
+            int64_t box_cap, int flags, cg_step_stats *stats);
+int cg_fetch_stats(cg_context *ctx, int64_t step_id, cg_step_stats *stats);
+/* Grid only (spatial.py:89-127 build_grid): no sweep, pool unchanged.  Fills
+ * the grid fields of stats (dims, origin, box_length, occupancy). */
+int cg_build_grid(cg_context *ctx, double interaction_radius, int64_t box_cap,
+                  cg_step_stats *stats);
+int cg_synchronize(cg_context *ctx);
+
+/* Grid of the last step: box_index per storage index (n), box_count in flat
+ * box order (prod(dims)).  Either pointer may be NULL. */
+int cg_grid_export(cg_context *ctx, int64_t *box_index, int64_t *box_count);
+/* Per-agent stencil candidates m and colliding pairs nk of the last step that
+ * ran with CG_STEP_RECORD (storage order). */
+int cg_record_export(cg_context *ctx, int32_t *m, int32_t *nk);
+
+/* Kernel-level drop-ins (host buffers in, host buffers out). */
+int cg_box_ids(cg_context *ctx, int64_t n, const void *px, const void *py, const void *pz,
+               double ox, double oy, double oz, double box_length,
+               int64_t dimx, int64_t dimy, int64_t dimz, int64_t *out);
+int cg_force_phase(cg_context *ctx, int64_t n, const void *px, const void *py, const void *pz,
+                   const void *radii, const void *adherence, const uint64_t *uid,
+                   const int64_t *box_index, int64_t dimx, int64_t dimy, int64_t dimz,
+                   const void *params7, void *out_dx, void *out_dy, void *out_dz,
+                   int64_t counters[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CELLGRID_B200_H */
