@@ -53,6 +53,8 @@ extern "C" {
 /* cg_set_option keys */
 #define CG_OPT_SUMMATION 1      /* 0 = uid order (bit-exact vs reference), 1 = stencil order */
 #define CG_OPT_BOX_ORDER 2      /* 0 = Morton (reference storage order), 1 = row-major */
+#define CG_OPT_SWEEP 3          /* 0 = thread-per-agent sweep, 1 = tiled shared-memory sweep */
+#define CG_OPT_TILE_CAP 4       /* staged agents per CTA of the tiled sweep (256..8192) */
 
 typedef struct cg_context cg_context;
 

@@ -21,6 +21,8 @@
 #include "common.cuh"
 #include "grid.cuh"
 #include "sweep.cuh"
+#include "sweep_tile.cuh"
+#include "sweep_proxy.cuh"
 
 using namespace cg;
 
@@ -37,6 +39,7 @@ struct Buffers {
     uint64_t *uid[2] = {nullptr, nullptr};
     void *disp[3] = {nullptr, nullptr, nullptr};
     int *key = nullptr, *rnk = nullptr, *tmp = nullptr, *idx = nullptr, *skey = nullptr;
+    float4 *prox = nullptr;
     int *rec_m = nullptr, *rec_nk = nullptr;
     unsigned long long *block_counters = nullptr;
 };
@@ -69,6 +72,9 @@ struct cg_context {
     Geometry geo{};
     bool morton = true;
     int summation = SUM_UID;
+    int sweep_impl = 2;                  // 0 = thread per agent, 1 = smem tiles, 2 = proxy (default)
+    int tile_cap = 2048;                 // staged agents per CTA
+    int debug_stop = 0;
     std::string err;
 };
 
@@ -99,10 +105,12 @@ static void free_agents(cg_context *c)
     void *ptrs[] = {b.pos[0][0], b.pos[0][1], b.pos[0][2], b.pos[1][0], b.pos[1][1], b.pos[1][2],
                     b.dia[0], b.dia[1], b.adh[0], b.adh[1], b.uid[0], b.uid[1],
                     b.disp[0], b.disp[1], b.disp[2], b.key, b.rnk, b.tmp, b.idx, b.skey,
-                    b.rec_m, b.rec_nk};
+                    b.rec_m, b.rec_nk, b.prox};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    unsigned long long *bc = b.block_counters;   // sized by launch shape, not by n: keep
     c->b = Buffers{};
+    c->b.block_counters = bc;
     c->cap = 0;
 }
 
@@ -120,6 +128,7 @@ static int alloc_agents(cg_context *c, int64_t cap)
     for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMalloc(&b.disp[a], fe));
     int **ints[] = {&b.key, &b.rnk, &b.tmp, &b.idx, &b.skey, &b.rec_m, &b.rec_nk};
     for (int **p : ints) CUDA_TRY(c, cudaMalloc(p, ie));
+    CUDA_TRY(c, cudaMalloc(&b.prox, sizeof(float4) * (size_t)cap));
     c->cap = cap;
     return CG_OK;
 }
@@ -239,16 +248,145 @@ static int build_grid(cg_context *c, double ir, int64_t box_cap, double origin[3
     scan_tile_sums<<<1, kThreads, 0, st>>>(ntiles, c->tile_sum);
     scan_add<<<cdiv(g.nb, kThreads), kThreads, 0, st>>>(g.nb, n, c->tile_sum, c->offset);
     place<<<nblk, kThreads, 0, st>>>(n, c->b.key, c->b.rnk, c->offset, c->b.tmp);
-    order_by_uid<<<nblk, kThreads, 0, st>>>(n, c->b.tmp, c->b.key, c->offset, c->b.uid[c->cur_attr],
-                                            c->b.idx, c->b.skey);
+    if (c->morton)
+        order_in_box<T, false><<<nblk, kThreads, 0, st>>>(n, c->b.tmp, c->b.key, c->offset,
+                                                          c->b.uid[c->cur_attr], z, c->b.idx, c->b.skey);
+    else
+        order_in_box<T, true><<<nblk, kThreads, 0, st>>>(n, c->b.tmp, c->b.key, c->offset,
+                                                         c->b.uid[c->cur_attr], z, c->b.idx, c->b.skey);
     LAUNCH_CHECK(c);
     c->launches += 6;
     return CG_OK;
 }
 
+// Pick the tile shape: largest core block whose expected halo population fits
+// comfortably in the staging capacity (overflowing tiles fall back to global
+// reads, so this only affects speed).
+static TileShape choose_tiles(const Geometry &g, int64_t n, int cap)
+{
+    const double rho = (double)n / (double)g.nb;
+    const int menu_xy[][2] = {{1, 1}, {1, 2}, {2, 2}, {2, 4}, {4, 4}, {4, 8}, {8, 8}};
+    const int menu_z[] = {4, 8, 16, 32};
+    TileShape best{1, 1, 4, 0, 0, 0, cap, 0, 0};
+    double best_core = -1.0;
+    for (auto &xy : menu_xy)
+        for (int tz : menu_z) {
+            const int tx = xy[0], ty = xy[1];
+            const int halo_boxes = (tx + 2) * (ty + 2) * (tz + 2);
+            if (halo_boxes > 1200) continue;
+            const double halo = rho * halo_boxes, core = rho * tx * ty * tz;
+            if (halo > 0.45 * cap) continue;
+            // prefer ~256-768 core agents; beyond that larger tiles add nothing
+            const double score = std::min(core, 768.0) + 1e-3 * core / halo;
+            if (score > best_core) {
+                best_core = score;
+                best = TileShape{tx, ty, tz, 0, 0, 0, cap, halo_boxes, 0};
+            }
+        }
+    best.ntx = cdiv(g.dimx, best.tx);
+    best.nty = cdiv(g.dimy, best.ty);
+    best.ntz = cdiv(g.dimz, best.tz);
+    best.max_halo_boxes = (best.tx + 2) * (best.ty + 2) * (best.tz + 2);
+    return best;
+}
+
+template <typename T, bool SORTED, int SUM, bool ZS>
+static cudaError_t launch_tile(cg_context *c, const TileArgs<T> &TA, int ntiles)
+{
+    const size_t smem = tile_smem_bytes<T>(TA.t);
+    auto kern = sweep_tile_kernel<T, SORTED, SUM, ZS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<ntiles, kThreads, smem, c->stream>>>(TA);
+    return cudaGetLastError();
+}
+
+template <typename T, bool SORTED, int SUM>
+static cudaError_t launch_tile_z(cg_context *c, const TileArgs<T> &TA, int ntiles)
+{
+    // row-major boxes are (z, uid)-ordered inside (order_in_box): z-window on
+    return TA.s.rank_of ? launch_tile<T, SORTED, SUM, false>(c, TA, ntiles)
+                        : launch_tile<T, SORTED, SUM, true>(c, TA, ntiles);
+}
+
+template <typename T, bool SORTED, int SUM, bool RM>
+static void launch_proxy_k(cg_context *c, const SweepArgs<T> &A, const ProxyArgs &P, int kscap)
+{
+    const int nblk = cdiv(A.n, kThreads);
+    if (kscap <= 32) {
+        auto k = sweep_proxy_kernel<T, SORTED, SUM, RM, 32>;
+        const int sm = 32 * kThreads * sizeof(int);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        k<<<nblk, kThreads, sm, c->stream>>>(A, P);
+    } else {
+        auto k = sweep_proxy_kernel<T, SORTED, SUM, RM, 64>;
+        const int sm = 64 * kThreads * sizeof(int);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        k<<<nblk, kThreads, sm, c->stream>>>(A, P);
+    }
+}
+
+template <typename T, bool SORTED>
+static void launch_proxy_s(cg_context *c, const SweepArgs<T> &A, const ProxyArgs &P, int kscap)
+{
+    const bool rm = A.rank_of == nullptr;
+    if (c->summation == SUM_UID) {
+        if (rm) launch_proxy_k<T, SORTED, SUM_UID, true>(c, A, P, kscap);
+        else launch_proxy_k<T, SORTED, SUM_UID, false>(c, A, P, kscap);
+    } else {
+        if (rm) launch_proxy_k<T, SORTED, SUM_STENCIL, true>(c, A, P, kscap);
+        else launch_proxy_k<T, SORTED, SUM_STENCIL, false>(c, A, P, kscap);
+    }
+}
+
 template <typename T>
 static int launch_sweep(cg_context *c, const SweepArgs<T> &A, bool sorted)
 {
+    if (c->sweep_impl == 2) {
+        const int nblk = cdiv(A.n, kThreads);
+        if (sorted)
+            make_proxy<T, true><<<nblk, kThreads, 0, c->stream>>>(A.n, A.g, A.idx, A.slot_key, A.flat_of,
+                                                                  A.x, A.y, A.z, A.d, c->b.prox);
+        else
+            make_proxy<T, false><<<nblk, kThreads, 0, c->stream>>>(A.n, A.g, A.idx, A.slot_key, A.flat_of,
+                                                                   A.x, A.y, A.z, A.d, c->b.prox);
+        LAUNCH_CHECK(c);
+        ProxyArgs P;
+        P.prox = c->b.prox;
+        // fp32 prefilter margin: every stored / derived fp32 coordinate is within
+        // a few ulp of E (box-local x/y, grid-relative z); 64 ulp(E) is used
+        const double E = A.g.L * (double)std::max(3, A.g.dimz + 2);
+        P.margin = (float)(64.0 * E * 5.9604644775390625e-8);
+        // survivors per agent ~ 4.19 * density (contact ball / box volume)
+        const double rho = (double)A.n / (double)A.g.nb;
+        const int kscap = 4.19 * rho <= 20.0 ? 32 : 64;
+        CUDA_TRY(c, cudaMemsetAsync(A.block_counters, 0, sizeof(unsigned long long) * 3 * kCounterSlots,
+                                    c->stream));
+        if (sorted) launch_proxy_s<T, true>(c, A, P, kscap);
+        else launch_proxy_s<T, false>(c, A, P, kscap);
+        LAUNCH_CHECK(c);
+        c->launches += 1;   // make_proxy (the sweep itself is counted by the caller)
+        return CG_OK;
+    }
+    if (c->sweep_impl == 1) {
+        TileArgs<T> TA;
+        TA.s = A;
+        TA.t = choose_tiles(A.g, A.n, c->tile_cap);
+        TA.t.debug_stop = c->debug_stop;
+        const long long nt = (long long)TA.t.ntx * TA.t.nty * TA.t.ntz;
+        if (nt >= INT32_MAX) return fail(c, CG_ERR_VALUE, "too many tiles");
+        CUDA_TRY(c, cudaMemsetAsync(A.block_counters, 0, sizeof(unsigned long long) * 3 * kCounterSlots,
+                                    c->stream));
+        cudaError_t e;
+        if (c->summation == SUM_UID)
+            e = sorted ? launch_tile_z<T, true, SUM_UID>(c, TA, (int)nt)
+                       : launch_tile_z<T, false, SUM_UID>(c, TA, (int)nt);
+        else
+            e = sorted ? launch_tile_z<T, true, SUM_STENCIL>(c, TA, (int)nt)
+                       : launch_tile_z<T, false, SUM_STENCIL>(c, TA, (int)nt);
+        CUDA_TRY(c, e);
+        return CG_OK;
+    }
     const int nblk = cdiv(A.n, kThreads);
     constexpr int KC = sizeof(T) == 8 ? 32 : 32;
     if (c->summation == SUM_UID) {
@@ -304,7 +442,7 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
     const int nblk = cdiv(n, kThreads);
-    if ((rc = ensure_block_counters(c, nblk))) return rc;
+    if ((rc = ensure_block_counters(c, std::max(nblk, kCounterSlots)))) return rc;
     SweepArgs<T> A;
     A.n = n;
     A.g = c->geo;
@@ -334,7 +472,8 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
     A.block_counters = c->b.block_counters;
     if ((rc = launch_sweep<T>(c, A, sort))) return rc;
     unsigned long long *stat = c->stat_dev + slot * kStatSlots;
-    reduce_counters<<<1, kThreads, 0, st>>>(nblk, c->b.block_counters, stat);
+    reduce_counters<<<1, kThreads, 0, st>>>(c->sweep_impl >= 1 ? kCounterSlots : nblk,
+                                            c->b.block_counters, stat);
     LAUNCH_CHECK(c);
     c->launches += 2;
     if (!freeze) c->cur_pos = 1 - cp;
@@ -474,6 +613,18 @@ int cg_set_option(cg_context *c, int key, int value)
     if (!c) return CG_ERR_VALUE;
     if (key == CG_OPT_SUMMATION && (value == SUM_UID || value == SUM_STENCIL)) {
         c->summation = value;
+        return CG_OK;
+    }
+    if (key == CG_OPT_SWEEP && value >= 0 && value <= 2) {
+        c->sweep_impl = value;
+        return CG_OK;
+    }
+    if (key == 99 && value >= 0 && value <= 2) {   // profiling aid (not in the header)
+        c->debug_stop = value;
+        return CG_OK;
+    }
+    if (key == CG_OPT_TILE_CAP && value >= 256 && value <= 8192) {
+        c->tile_cap = value;
         return CG_OK;
     }
     if (key == CG_OPT_BOX_ORDER && (value == 0 || value == 1)) {
@@ -687,6 +838,14 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     c->geo = g;
     c->morton = false;   // kernel-level call: row-major keys taken from box_index
     c->table_dims[0] = 0;
+    // no box_length is given at this level, so use the thread-per-agent sweep
+    // (the tiled sweep's prefilter needs L)
+    struct Restore {
+        cg_context *c;
+        int v;
+        ~Restore() { c->sweep_impl = v; }
+    } restore{c, c->sweep_impl};
+    c->sweep_impl = 0;
     long long *dbox = nullptr;
     CUDA_TRY(c, cudaMallocAsync(&dbox, sizeof(long long) * n, st));
     CUDA_TRY(c, cudaMemcpyAsync(dbox, box_index, sizeof(long long) * n, cudaMemcpyHostToDevice, st));
@@ -703,10 +862,10 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     scan_tile_sums<<<1, kThreads, 0, st>>>(ntiles, c->tile_sum);
     scan_add<<<cdiv(g.nb, kThreads), kThreads, 0, st>>>(g.nb, nn, c->tile_sum, c->offset);
     place<<<nblk, kThreads, 0, st>>>(nn, c->b.key, c->b.rnk, c->offset, c->b.tmp);
-    order_by_uid<<<nblk, kThreads, 0, st>>>(nn, c->b.tmp, c->b.key, c->offset, c->b.uid[0],
-                                            c->b.idx, c->b.skey);
+    order_in_box<double, false><<<nblk, kThreads, 0, st>>>(nn, c->b.tmp, c->b.key, c->offset,
+                                                           c->b.uid[0], nullptr, c->b.idx, c->b.skey);
     LAUNCH_CHECK(c);
-    if ((rc = ensure_block_counters(c, nblk))) return rc;
+    if ((rc = ensure_block_counters(c, std::max(nblk, kCounterSlots)))) return rc;
     double p5[5];
     for (int k = 0; k < 5; ++k)
         p5[k] = c->prec == CG_FP64 ? ((const double *)params7)[k] : (double)((const float *)params7)[k];
@@ -731,7 +890,8 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
         A.block_counters = c->b.block_counters;
         if ((rc = launch_sweep<float>(c, A, false))) return rc;
     }
-    reduce_counters<<<1, kThreads, 0, st>>>(nblk, c->b.block_counters, stat);
+    reduce_counters<<<1, kThreads, 0, st>>>(c->sweep_impl >= 1 ? kCounterSlots : nblk,
+                                            c->b.block_counters, stat);
     LAUNCH_CHECK(c);
     unsigned long long h[kStatSlots];
     CUDA_TRY(c, cudaMemcpyAsync(h, stat, sizeof h, cudaMemcpyDeviceToHost, st));

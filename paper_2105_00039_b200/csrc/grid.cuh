@@ -6,7 +6,8 @@
 //   K1 bbox_partial/bbox_final   pool.py:102-110 max_diameter + bounding_box
 //   K2 box_keys                  kernels.py:107-129 box ids, warp-aggregated counts
 //   K3 scan_*                    exclusive prefix sum of counts -> box offsets
-//   K4 place + order_by_uid      counting-sort scatter; members of a box ordered by uid
+//   K4 place + order_in_box      counting-sort scatter; members of a box ordered by uid
+//                                (Morton order) or by (z, uid) (row-major order)
 //   K5 morton_table              box -> Morton rank (boxes visited in Z-order)
 //   K4b gather_records           apply the permutation (storage re-sort)
 #pragma once
@@ -236,12 +237,15 @@ __global__ void place(int n, const int *__restrict__ key, const int *__restrict_
     if (i < n) tmp[offset[key[i]] + rank_in_box[i]] = i;
 }
 
-// Members of a box are re-ranked by uid so slot order (and therefore the
-// summation order of the sweep and the storage order after a sort) is a pure
-// function of the population -- morton.py:67-74 (lexsort by (code, uid)).
-__global__ void order_by_uid(int n, const int *__restrict__ tmp, const int *__restrict__ key,
+// Members of a box are re-ranked so slot order (the summation order of the
+// sweep and the storage order after a sort) is a pure function of the
+// population: by uid (Morton box order == the reference's lexsort((uid, code)),
+// morton.py:67-74) or, for row-major box order, by (z, uid) so that every
+// 3-box z-run of the stencil is z-sorted (the sweep's z-window relies on it).
+template <typename T, bool BY_Z>
+__global__ void order_in_box(int n, const int *__restrict__ tmp, const int *__restrict__ key,
                              const int *__restrict__ offset, const uint64_t *__restrict__ uid,
-                             int *__restrict__ idx, int *__restrict__ skey)
+                             const T *__restrict__ zc, int *__restrict__ idx, int *__restrict__ skey)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
@@ -250,7 +254,16 @@ __global__ void order_by_uid(int n, const int *__restrict__ tmp, const int *__re
     const int o0 = offset[k], o1 = offset[k + 1];
     const uint64_t u = uid[i];
     int q = 0;
-    for (int t = o0; t < o1; ++t) q += (__ldg(uid + __ldg(tmp + t)) < u);
+    if (BY_Z) {
+        const T zi = zc[i];
+        for (int t = o0; t < o1; ++t) {
+            const int j = __ldg(tmp + t);
+            const T zj = zc[j];
+            q += (zj < zi) || (zj == zi && __ldg(uid + j) < u);
+        }
+    } else {
+        for (int t = o0; t < o1; ++t) q += (__ldg(uid + __ldg(tmp + t)) < u);
+    }
     idx[o0 + q] = i;
     skey[o0 + q] = k;
 }

@@ -27,11 +27,14 @@ def _native():
     return _native
 
 
-def _ctx(dtype, summation="uid", box_order="morton"):
+def _ctx(dtype, summation="uid", box_order="morton", sweep="tile", tile_cap=None):
     N = _native()
     ctx = N.Context(0, dtype)
     ctx.set_option(N.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[summation])
     ctx.set_option(N.CG_OPT_BOX_ORDER, {"morton": 0, "rowmajor": 1}[box_order])
+    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "tile": 1}[sweep])
+    if tile_cap:
+        ctx.set_option(N.CG_OPT_TILE_CAP, tile_cap)
     return ctx
 
 
@@ -67,16 +70,20 @@ def _reference_state(g, k):
             g["in_adh"][order], uid]
 
 
+@pytest.mark.parametrize("sweep", ["tile", "agent", "tile-overflow"])
 @pytest.mark.parametrize("summation", ["uid", "stencil"])
 @pytest.mark.parametrize("name", golden_names())
-def test_golden_morton(cuda_required, name, summation):
+def test_golden_morton(cuda_required, name, summation, sweep):
     """uid mode chains all steps on the device (bit-exact end to end); stencil
     mode restarts every step from the reference's state, because its last-ulp
     differences legitimately move later bounding boxes."""
     g = load_golden(name)
     dt = g["in_px"].dtype
     N = _native()
-    ctx = _ctx(dt, summation)
+    if sweep == "tile-overflow":    # staging capacity too small: global-memory fallback
+        ctx = _ctx(dt, summation, sweep="tile", tile_cap=256)
+    else:
+        ctx = _ctx(dt, summation, sweep=sweep)
     every = int(g["sort_every"])
     for k in range(int(g["steps"])):
         s = "s%d_" % k

@@ -1,0 +1,32 @@
+"""Minimal driver for ncu captures: upload a config and run a few steps.
+
+usage: python tools/one_step.py <c1|c2|c4|c3_<d>>[f] [summation 0|1] [box_order 0|1] [steps]
+(env SWEEP=0|1 selects the sweep kernel)
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+from paper_2105_00039_b200 import _native, workloads  # noqa: E402
+from paper_2105_00039_b200.pool import PrecisionMode  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c4"
+summ = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+order = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+steps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+pm = PrecisionMode.FP32 if name.endswith("f") else PrecisionMode.FP64
+base = name.rstrip("f")
+makers = {"c1": lambda: workloads.c1(pm), "c2": lambda: workloads.c2(pm),
+          "c4": lambda: workloads.c4(pm)}
+pool = makers.get(base, lambda: workloads.c3(float(base[3:]), pm))()
+ctx = _native.Context(0, pool.dtype)
+ctx.set_option(_native.CG_OPT_SUMMATION, summ)
+ctx.set_option(_native.CG_OPT_BOX_ORDER, order)
+ctx.set_option(_native.CG_OPT_SWEEP, int(os.environ.get("SWEEP", "2")))
+ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence,
+           pool.uid)
+for k in range(steps):
+    st = ctx.step(np.array([2.0, 1.0, 0.01, 3.0, 1.0]), None, 1 << 24, 1)
+print("force %.3f ms total %.3f ms" % (st.t_force_ms, st.t_total_ms))
