@@ -27,12 +27,12 @@ def _native():
     return _native
 
 
-def _ctx(dtype, summation="uid", box_order="morton", sweep="tile", tile_cap=None):
+def _ctx(dtype, summation="uid", box_order="morton", sweep="proxy", tile_cap=None):
     N = _native()
     ctx = N.Context(0, dtype)
     ctx.set_option(N.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[summation])
     ctx.set_option(N.CG_OPT_BOX_ORDER, {"morton": 0, "rowmajor": 1}[box_order])
-    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "tile": 1}[sweep])
+    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "tile": 1, "proxy": 2}[sweep])
     if tile_cap:
         ctx.set_option(N.CG_OPT_TILE_CAP, tile_cap)
     return ctx
@@ -70,7 +70,7 @@ def _reference_state(g, k):
             g["in_adh"][order], uid]
 
 
-@pytest.mark.parametrize("sweep", ["tile", "agent", "tile-overflow"])
+@pytest.mark.parametrize("sweep", ["proxy", "tile", "agent", "tile-overflow"])
 @pytest.mark.parametrize("summation", ["uid", "stencil"])
 @pytest.mark.parametrize("name", golden_names())
 def test_golden_morton(cuda_required, name, summation, sweep):
@@ -126,12 +126,14 @@ def test_golden_morton(cuda_required, name, summation, sweep):
     ctx.close()
 
 
-@pytest.mark.parametrize("name", ["rand600_s0_f64", "multistep_f64", "hetero_f64", "c1_f32"])
-def test_golden_rowmajor_box_order(cuda_required, name):
+@pytest.mark.parametrize("sweep", ["proxy", "tile"])
+@pytest.mark.parametrize("name", ["rand600_s0_f64", "multistep_f64", "hetero_f64", "c1_f32",
+                                  "dense3000_f64", "faces_f64"])
+def test_golden_rowmajor_box_order(cuda_required, name, sweep):
     """Row-major box order: identical physics keyed by uid (storage order differs)."""
     g = load_golden(name)
     N = _native()
-    ctx = _ctx(g["in_px"].dtype, "uid", "rowmajor")
+    ctx = _ctx(g["in_px"].dtype, "uid", "rowmajor", sweep=sweep)
     ctx.upload(g["in_px"], g["in_py"], g["in_pz"], g["in_diam"], g["in_adh"], g["in_uid"])
     every = int(g["sort_every"])
     for k in range(int(g["steps"])):
