@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--config", default="c4", help="c4 (default), c2, c1, c3_<density>")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--summation", default="stencil", choices=["uid", "stencil"])
-    ap.add_argument("--box-order", default="rowmajor", choices=["morton", "rowmajor"])
+    ap.add_argument("--relayout-every", type=int, default=1,
+                    help="move records into slot order on every k-th sort step")
     ap.add_argument("--sort-every", type=int, default=1)
     ap.add_argument("--freeze", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -242,7 +243,7 @@ def main():
                            | (_native.CG_STEP_FREEZE if args.freeze else 0))
     ctx = _native.Context(local, pool.dtype)
     ctx.set_option(_native.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[args.summation])
-    ctx.set_option(_native.CG_OPT_BOX_ORDER, {"morton": 0, "rowmajor": 1}[args.box_order])
+    ctx.set_option(_native.CG_OPT_RELAYOUT_EVERY, args.relayout_every)
     ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence,
                pool.uid)
     params = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
@@ -284,7 +285,7 @@ def main():
                        displacement_x=pin(pool.displacement_x), displacement_y=pin(pool.displacement_y),
                        displacement_z=pin(pool.displacement_z))
         cfg = eng.SimulationConfig(strategy=eng.Gpu(device=local, summation=args.summation,
-                                                    box_order=args.box_order),
+                                                    relayout_every=args.relayout_every),
                                    precision=PrecisionMode.FP64 if args.precision == "fp64" else PrecisionMode.FP32,
                                    morton_sort_every=args.sort_every, freeze_displacement=args.freeze)
         eng.step(hp, cfg, 0)                       # warm the context
@@ -317,12 +318,12 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
         "config": {"workload": desc, "agents_per_gpu": n, "sort_every": args.sort_every,
-                   "freeze": args.freeze, "summation": args.summation, "box_order": args.box_order,
+                   "freeze": args.freeze, "summation": args.summation, "relayout_every": args.relayout_every,
                    "l2": "inputs larger than L2 (%.0f MB of agent state per GPU)" % (n * (6 * np.dtype(pool.dtype).itemsize + 8) / 1e6),
                    "parallelism": "single GPU" if world == 1 else "replicas x%d (no halo exchange)" % world},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.precision),
-                     "kernel": "sweep_kernel", "alg_bytes_per_agent": bal,
+                     "kernel": "sweep7_kernel", "alg_bytes_per_agent": bal,
                      "kernel_ms": t_force, "peak_source": peak_src},
         "step_roofline_frac": n * bal / (ms * 1e-3) / 1e9 / peak,
         "pair_interactions_per_s": evals * world / (ms * 1e-3),

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CG_ABI_VERSION 1
+#define CG_ABI_VERSION 2
 
 /* status codes */
 #define CG_OK 0
@@ -52,9 +52,8 @@ extern "C" {
 
 /* cg_set_option keys */
 #define CG_OPT_SUMMATION 1      /* 0 = uid order (bit-exact vs reference), 1 = stencil order */
-#define CG_OPT_BOX_ORDER 2      /* 0 = Morton (reference storage order), 1 = row-major */
-#define CG_OPT_SWEEP 3          /* 0 = thread-per-agent sweep, 1 = tiled shared-memory sweep */
-#define CG_OPT_TILE_CAP 4       /* staged agents per CTA of the tiled sweep (256..8192) */
+#define CG_OPT_SWEEP 3          /* 0 = reference-order thread-per-agent sweep, 1 = production sweep (default) */
+#define CG_OPT_RELAYOUT_EVERY 4 /* move the records into slot order on every k-th sort step (k >= 1, default 1) */
 
 typedef struct cg_context cg_context;
 
@@ -86,8 +85,9 @@ void *cg_stream(cg_context *ctx);
 /* Columns in the context precision; uid is uint64.  n may be 0. */
 int cg_upload(cg_context *ctx, int64_t n, const void *px, const void *py, const void *pz,
               const void *diameter, const void *adherence, const uint64_t *uid);
-/* Any pointer may be NULL to skip that column.  Storage order is the device
- * order, which equals the reference's after a Morton-sorted step. */
+/* Any pointer may be NULL to skip that column.  Columns come back in the
+ * reference's storage order: upload order until the first sort step, then the
+ * (Morton code, uid) order of the last sort step (morton.py:67-74). */
 int cg_download(cg_context *ctx, void *px, void *py, void *pz, void *diameter,
                 void *adherence, uint64_t *uid, void *dx, void *dy, void *dz);
 int64_t cg_count(const cg_context *ctx);

@@ -3,13 +3,24 @@
 //
 // One context = one agent population resident in the HBM of one B200.  A step
 // (reference engine.py:279-341) is:
-//   K1 bbox -> host geometry (spatial.py:99-116, bit-exact f64) -> [K5 Morton
-//   table if dims changed] -> K2 box keys + warp-aggregated counts -> K3 scan ->
-//   K4 place + uid order -> [K4b gather when the Z-order sort is due] ->
-//   sweep (force, gate, cap, apply) -> counter reduction.
-// The only host round trip is the 7-double bbox readback (needed to size the
-// grid and to raise GridOverflowError before anything is modified, exactly
-// where the reference raises).
+//   bbox (from the previous sweep's reduction slots; a standalone pass only
+//   after an upload) -> host geometry (spatial.py:99-116, exact f64) ->
+//   box_keys (+ warp-aggregated counts) -> scan_lookback -> place ->
+//   order_gather (CSR slots by (box, z, uid), fp32 proxies; on a relayout
+//   step the records themselves move into slot order) -> sweep7 (force,
+//   gate, cap, apply, counters, next bbox) -> finish_step (fold the slots).
+// The only host round trip is the 7-double bbox readback: it sizes the grid
+// and raises GridOverflowError before anything is modified, exactly where the
+// reference raises.
+//
+// Storage order.  The reference re-sorts its pool into (Morton code, uid)
+// order on every sort step (engine.py:305-309, morton.py:67-74); only the
+// pool's storage order observes that.  Here the records move into the
+// device's slot order on relayout steps (every `relayout_every`-th sort step)
+// and the reference's order is kept as a permutation `pres` (storage index
+// -> reference storage position), materialised only when the host downloads
+// or exports -- so every download returns exactly the reference's pool.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -21,8 +32,7 @@
 #include "common.cuh"
 #include "grid.cuh"
 #include "sweep.cuh"
-#include "sweep_tile.cuh"
-#include "sweep_proxy.cuh"
+#include "sweep7.cuh"
 
 using namespace cg;
 
@@ -30,7 +40,10 @@ namespace {
 
 constexpr int kStatSlots = 8;        // per step: occupied, maxocc, evals, cands, ndeg
 constexpr int kRing = 64;            // pinned stats ring (steps in flight)
-constexpr int kBboxBlocks = 148 * 4; // grid-stride bbox reduction: 4 CTAs per SM
+constexpr int kBboxBlocks = 148 * 4;
+constexpr int kMaxCounterBlocks = 1 << 20;
+
+enum { PRES_IDENTITY = 0, PRES_VALID = 1, PRES_PENDING = 2 };
 
 struct Buffers {
     void *pos[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
@@ -38,10 +51,13 @@ struct Buffers {
     void *adh[2] = {nullptr, nullptr};
     uint64_t *uid[2] = {nullptr, nullptr};
     void *disp[3] = {nullptr, nullptr, nullptr};
-    int *key = nullptr, *rnk = nullptr, *tmp = nullptr, *idx = nullptr, *skey = nullptr;
-    float4 *prox = nullptr;
+    int2 *key_rank = nullptr;
+    int *tmp = nullptr, *idx = nullptr, *skey = nullptr, *pres = nullptr;
     int *rec_m = nullptr, *rec_nk = nullptr;
-    unsigned long long *block_counters = nullptr;
+    float *prox = nullptr;           // Proxies: xy (4 floats per slot pair) then z
+    Proxies P() const { return Proxies{prox, prox + 4 * pairs}; }
+    int64_t pairs = 0;
+    void *stage = nullptr;           // download staging (n x 8 B)
 };
 
 }  // namespace
@@ -54,27 +70,36 @@ struct cg_context {
     int64_t n = 0, cap = 0;
     Buffers b;
     int cur_pos = 0, cur_attr = 0;
-    // grid
-    int64_t box_cap = 0;                 // allocated box capacity
-    int *count = nullptr, *offset = nullptr, *tile_sum = nullptr, *mrank = nullptr, *minv = nullptr;
+    // boxes
+    int64_t box_cap = 0;
+    int *count = nullptr, *offset = nullptr, *mrank = nullptr, *minv = nullptr, *moff = nullptr;
+    unsigned long long *scan_status = nullptr;   // (tiles + 2) words; the last two are tickets
+    int64_t scan_tiles_cap = 0;
     int table_dims[3] = {0, 0, 0};
-    int64_t blockctr_cap = 0;
-    double *bbox_partial = nullptr, *bbox_dev = nullptr;
-    double *bbox_host = nullptr;         // pinned
-    unsigned long long *stat_dev = nullptr;   // kRing * kStatSlots
-    unsigned long long *stat_host = nullptr;  // pinned mirror
+    // per-step reductions
+    unsigned long long *slots = nullptr;
+    unsigned long long *maxd_enc = nullptr;
+    unsigned long long *block_counters = nullptr;   // reference-order sweep only
+    double *bbox_dev = nullptr, *bbox_host = nullptr;
+    bool bbox_valid = false;
+    double max_diam = 0.0;
+    unsigned long long *stat_dev = nullptr, *stat_host = nullptr;
     cg_step_stats ring[kRing];
     cudaEvent_t ev[kRing][5];
     int64_t steps_done = 0;
-    int64_t launches = 0;                // kernels launched by this context
-    // last step
-    bool have_grid = false, last_sorted = false, last_record = false;
+    int64_t launches = 0;
+    // grid / layout state
     Geometry geo{};
-    bool morton = true;
+    BoxDecode bd{};
+    bool have_grid = false;
+    bool relaid = false;          // storage == slot order of the current grid
+    int pres_state = PRES_IDENTITY;
+    bool last_record = false;
+    int64_t sort_steps = 0;
+    // options
     int summation = SUM_UID;
-    int sweep_impl = 2;                  // 0 = thread per agent, 1 = smem tiles, 2 = proxy (default)
-    int tile_cap = 2048;                 // staged agents per CTA
-    int debug_stop = 0;
+    int sweep_impl = 1;           // 0 = reference-order thread per agent, 1 = sweep7
+    int relayout_every = 1;       // relayout on every k-th sort step (1 = every sort step)
     std::string err;
 };
 
@@ -104,13 +129,11 @@ static void free_agents(cg_context *c)
     Buffers &b = c->b;
     void *ptrs[] = {b.pos[0][0], b.pos[0][1], b.pos[0][2], b.pos[1][0], b.pos[1][1], b.pos[1][2],
                     b.dia[0], b.dia[1], b.adh[0], b.adh[1], b.uid[0], b.uid[1],
-                    b.disp[0], b.disp[1], b.disp[2], b.key, b.rnk, b.tmp, b.idx, b.skey,
-                    b.rec_m, b.rec_nk, b.prox};
+                    b.disp[0], b.disp[1], b.disp[2], b.key_rank, b.tmp, b.idx, b.skey, b.pres,
+                    b.rec_m, b.rec_nk, b.prox, b.stage};
     for (void *p : ptrs)
         if (p) cudaFree(p);
-    unsigned long long *bc = b.block_counters;   // sized by launch shape, not by n: keep
     c->b = Buffers{};
-    c->b.block_counters = bc;
     c->cap = 0;
 }
 
@@ -126,9 +149,13 @@ static int alloc_agents(cg_context *c, int64_t cap)
         CUDA_TRY(c, cudaMalloc(&b.uid[k], sizeof(uint64_t) * (size_t)cap));
     }
     for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMalloc(&b.disp[a], fe));
-    int **ints[] = {&b.key, &b.rnk, &b.tmp, &b.idx, &b.skey, &b.rec_m, &b.rec_nk};
+    CUDA_TRY(c, cudaMalloc(&b.key_rank, sizeof(int2) * (size_t)cap));
+    int **ints[] = {&b.tmp, &b.idx, &b.skey, &b.pres, &b.rec_m, &b.rec_nk};
     for (int **p : ints) CUDA_TRY(c, cudaMalloc(p, ie));
-    CUDA_TRY(c, cudaMalloc(&b.prox, sizeof(float4) * (size_t)cap));
+    b.pairs = cap / 2 + 8;   // the sweep may read a few pairs past n
+    CUDA_TRY(c, cudaMalloc(&b.prox, sizeof(float) * 6 * (size_t)b.pairs));
+    CUDA_TRY(c, cudaMemset(b.prox, 0, sizeof(float) * 6 * (size_t)b.pairs));
+    CUDA_TRY(c, cudaMalloc(&b.stage, 8 * (size_t)cap));
     c->cap = cap;
     return CG_OK;
 }
@@ -136,26 +163,21 @@ static int alloc_agents(cg_context *c, int64_t cap)
 static int ensure_boxes(cg_context *c, int64_t nb)
 {
     if (nb <= c->box_cap) return CG_OK;
-    int64_t want = nb + nb / 4 + 1024;
-    int *ptrs[] = {c->count, c->offset, c->tile_sum, c->mrank, c->minv};
+    const int64_t want = nb + nb / 4 + 1024;
+    int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->moff};
     for (int *p : ptrs)
         if (p) cudaFree(p);
+    if (c->scan_status) cudaFree(c->scan_status);
     CUDA_TRY(c, cudaMalloc(&c->count, sizeof(int) * want));
+    CUDA_TRY(c, cudaMemsetAsync(c->count, 0, sizeof(int) * want, c->stream));   // the scan keeps it zero
     CUDA_TRY(c, cudaMalloc(&c->offset, sizeof(int) * (want + 1)));
-    CUDA_TRY(c, cudaMalloc(&c->tile_sum, sizeof(int) * (cdiv(want, kScanTile) + 1)));
     CUDA_TRY(c, cudaMalloc(&c->mrank, sizeof(int) * want));
     CUDA_TRY(c, cudaMalloc(&c->minv, sizeof(int) * want));
+    CUDA_TRY(c, cudaMalloc(&c->moff, sizeof(int) * (want + 1)));
+    c->scan_tiles_cap = cdiv(want, kScanTile) + 1;
+    CUDA_TRY(c, cudaMalloc(&c->scan_status, sizeof(unsigned long long) * (c->scan_tiles_cap + 2)));
     c->box_cap = want;
     c->table_dims[0] = c->table_dims[1] = c->table_dims[2] = 0;
-    return CG_OK;
-}
-
-static int ensure_block_counters(cg_context *c, int64_t nblocks)
-{
-    if (nblocks <= c->blockctr_cap) return CG_OK;
-    if (c->b.block_counters) cudaFree(c->b.block_counters);
-    CUDA_TRY(c, cudaMalloc(&c->b.block_counters, sizeof(unsigned long long) * 3 * nblocks));
-    c->blockctr_cap = nblocks;
     return CG_OK;
 }
 
@@ -181,7 +203,7 @@ static int host_geometry(cg_context *c, const double bb[7], double ir, int64_t b
                     "sparse for box_length %g",
                     (long long)dims64[0], (long long)dims64[1], (long long)dims64[2],
                     (long long)nb, (long long)box_cap, L);
-    if (nb >= (int64_t)INT32_MAX)
+    if (nb >= (int64_t)INT32_MAX / 2)
         return fail(c, CG_ERR_GRID_OVERFLOW, "grid of %lld boxes exceeds the int32 box index range",
                     (long long)nb);
     g.L = L;
@@ -193,6 +215,16 @@ static int host_geometry(cg_context *c, const double bb[7], double ir, int64_t b
     g.dimz = (int)dims64[2];
     g.nb = (int)nb;
     return CG_OK;
+}
+
+static BoxDecode make_decode(const Geometry &g)
+{
+    BoxDecode bd;
+    bd.by_z = FastDiv((unsigned)g.dimz);
+    bd.by_y = FastDiv((unsigned)g.dimy);
+    bd.dimz = g.dimz;
+    bd.dimy = g.dimy;
+    return bd;
 }
 
 template <typename T>
@@ -208,28 +240,48 @@ static Params<T> make_params(const double p[5])
     return q;
 }
 
-// Grid build (K1..K4) on the current storage: leaves count/offset/key/rnk/idx/skey.
+// Exclusive scan of the per-box counts (grid) or of the counts in Morton
+// box order (presentation).  stat may be null.
+static int launch_scan(cg_context *c, bool morton, int nb, int *out, unsigned long long *stat)
+{
+    const int ntiles = cdiv(nb, kScanTile);
+    CUDA_TRY(c, cudaMemsetAsync(c->scan_status, 0, sizeof(unsigned long long) * ntiles, c->stream));
+    unsigned *ticket = reinterpret_cast<unsigned *>(c->scan_status + c->scan_tiles_cap);
+    CUDA_TRY(c, cudaMemsetAsync(ticket, 0, sizeof(unsigned), c->stream));
+    ScanState S{c->scan_status, ticket};
+    if (morton)
+        scan_lookback<true><<<ntiles, kThreads, 0, c->stream>>>(nb, nullptr, c->offset, c->minv, out, S, stat);
+    else
+        scan_lookback<false><<<ntiles, kThreads, 0, c->stream>>>(nb, c->count, nullptr, nullptr, out, S, stat);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    return CG_OK;
+}
+
+// Standalone bbox of the stored positions into bbox_host (synchronous).
 template <typename T>
-static int build_grid(cg_context *c, double ir, int64_t box_cap, double origin[3], int64_t dims64[3])
+static int standalone_bbox(cg_context *c)
 {
     const int n = (int)c->n;
     cudaStream_t st = c->stream;
-    T *x = (T *)c->b.pos[c->cur_pos][0], *y = (T *)c->b.pos[c->cur_pos][1],
-      *z = (T *)c->b.pos[c->cur_pos][2], *d = (T *)c->b.dia[c->cur_attr];
-    const int nbb = std::min(kBboxBlocks, cdiv(n, kThreads));
-    bbox_partial<T><<<nbb, kThreads, 0, st>>>(n, x, y, z, d, c->bbox_partial);
-    bbox_final<<<1, 32, 0, st>>>(nbb, c->bbox_partial, c->bbox_dev);
+    T *x = (T *)c->b.pos[c->cur_pos][0], *y = (T *)c->b.pos[c->cur_pos][1], *z = (T *)c->b.pos[c->cur_pos][2];
+    bbox_slots<T><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(n, x, y, z, c->slots);
+    finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, nullptr, c->bbox_dev, FINISH_BBOX);
     LAUNCH_CHECK(c);
     c->launches += 2;
     CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));
-    Geometry g;
-    int rc = host_geometry(c, c->bbox_host, ir, box_cap, g, dims64, origin);
-    if (rc) return rc;
-    if ((rc = ensure_boxes(c, g.nb))) return rc;
-    c->geo = g;
-    if (c->morton && (c->table_dims[0] != g.dimx || c->table_dims[1] != g.dimy ||
-                      c->table_dims[2] != g.dimz)) {
+    c->bbox_valid = true;
+    return CG_OK;
+}
+
+// The reference's storage order for the current grid (see header comment).
+static int materialize_presentation(cg_context *c)
+{
+    if (c->pres_state != PRES_PENDING) return CG_OK;
+    const Geometry &g = c->geo;
+    cudaStream_t st = c->stream;
+    if (c->table_dims[0] != g.dimx || c->table_dims[1] != g.dimy || c->table_dims[2] != g.dimz) {
         morton_table<<<std::min(cdiv(g.nb, kThreads), 148 * 16), kThreads, 0, st>>>(g, c->mrank, c->minv);
         LAUNCH_CHECK(c);
         c->launches += 1;
@@ -237,166 +289,202 @@ static int build_grid(cg_context *c, double ir, int64_t box_cap, double origin[3
         c->table_dims[1] = g.dimy;
         c->table_dims[2] = g.dimz;
     }
-    CUDA_TRY(c, cudaMemsetAsync(c->count, 0, sizeof(int) * g.nb, st));
-    const int nblk = cdiv(n, kThreads);
-    box_keys<T><<<nblk, kThreads, 0, st>>>(n, g, x, y, z, c->morton ? c->mrank : nullptr, c->count,
-                                           c->b.key, c->b.rnk);
-    const int ntiles = cdiv(g.nb, kScanTile);
-    unsigned long long *stat = c->stat_dev + (c->steps_done % kRing) * kStatSlots;
-    CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
-    scan_tiles<<<ntiles, kThreads, 0, st>>>(g.nb, c->count, c->offset, c->tile_sum, stat);
-    scan_tile_sums<<<1, kThreads, 0, st>>>(ntiles, c->tile_sum);
-    scan_add<<<cdiv(g.nb, kThreads), kThreads, 0, st>>>(g.nb, n, c->tile_sum, c->offset);
-    place<<<nblk, kThreads, 0, st>>>(n, c->b.key, c->b.rnk, c->offset, c->b.tmp);
-    if (c->morton)
-        order_in_box<T, false><<<nblk, kThreads, 0, st>>>(n, c->b.tmp, c->b.key, c->offset,
-                                                          c->b.uid[c->cur_attr], z, c->b.idx, c->b.skey);
-    else
-        order_in_box<T, true><<<nblk, kThreads, 0, st>>>(n, c->b.tmp, c->b.key, c->offset,
-                                                         c->b.uid[c->cur_attr], z, c->b.idx, c->b.skey);
+    int rc = launch_scan(c, true, g.nb, c->moff, nullptr);
+    if (rc) return rc;
+    const int n = (int)c->n;
+    presentation<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, c->b.skey, c->relaid ? nullptr : c->b.idx,
+                                                          c->offset, c->mrank, c->moff,
+                                                          c->b.uid[c->cur_attr], c->b.pres);
     LAUNCH_CHECK(c);
-    c->launches += 6;
+    c->launches += 1;
+    c->pres_state = PRES_VALID;
     return CG_OK;
 }
 
-// Pick the tile shape: largest core block whose expected halo population fits
-// comfortably in the staging capacity (overflowing tiles fall back to global
-// reads, so this only affects speed).
-static TileShape choose_tiles(const Geometry &g, int64_t n, int cap)
+// Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
+// idx (or, when relayout, the records in slot order in the alternate buffers).
+template <typename T>
+static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, double origin[3],
+                      int64_t dims64[3])
 {
-    const double rho = (double)n / (double)g.nb;
-    const int menu_xy[][2] = {{1, 1}, {1, 2}, {2, 2}, {2, 4}, {4, 4}, {4, 8}, {8, 8}};
-    const int menu_z[] = {4, 8, 16, 32};
-    TileShape best{1, 1, 4, 0, 0, 0, cap, 0, 0};
-    double best_core = -1.0;
-    for (auto &xy : menu_xy)
-        for (int tz : menu_z) {
-            const int tx = xy[0], ty = xy[1];
-            const int halo_boxes = (tx + 2) * (ty + 2) * (tz + 2);
-            if (halo_boxes > 1200) continue;
-            const double halo = rho * halo_boxes, core = rho * tx * ty * tz;
-            if (halo > 0.45 * cap) continue;
-            // prefer ~256-768 core agents; beyond that larger tiles add nothing
-            const double score = std::min(core, 768.0) + 1e-3 * core / halo;
-            if (score > best_core) {
-                best_core = score;
-                best = TileShape{tx, ty, tz, 0, 0, 0, cap, halo_boxes, 0};
-            }
-        }
-    best.ntx = cdiv(g.dimx, best.tx);
-    best.nty = cdiv(g.dimy, best.ty);
-    best.ntz = cdiv(g.dimz, best.tz);
-    best.max_halo_boxes = (best.tx + 2) * (best.ty + 2) * (best.tz + 2);
-    return best;
+    const int n = (int)c->n;
+    cudaStream_t st = c->stream;
+    int rc;
+    if (!c->bbox_valid) {
+        if ((rc = standalone_bbox<T>(c))) return rc;
+    } else {
+        CUDA_TRY(c, cudaStreamSynchronize(st));   // the previous step's bbox readback
+    }
+    Geometry g;
+    if ((rc = host_geometry(c, c->bbox_host, ir, box_cap, g, dims64, origin))) return rc;
+    const int slot = (int)(c->steps_done % kRing);
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][0], st));
+    // the previous grid is about to be overwritten: keep its presentation order
+    if ((rc = materialize_presentation(c))) return rc;
+    if ((rc = ensure_boxes(c, g.nb))) return rc;
+    c->geo = g;
+    c->bd = make_decode(g);
+    unsigned long long *stat = c->stat_dev + slot * kStatSlots;
+    CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
+    const int nblk = cdiv(n, kThreads);
+    T *x = (T *)c->b.pos[c->cur_pos][0], *y = (T *)c->b.pos[c->cur_pos][1], *z = (T *)c->b.pos[c->cur_pos][2];
+    box_keys<T><<<nblk, kThreads, 0, st>>>(n, g, x, y, z, c->count, c->b.key_rank);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    if ((rc = launch_scan(c, false, g.nb, c->offset, stat))) return rc;
+    place<<<nblk, kThreads, 0, st>>>(n, c->b.key_rank, c->offset, c->b.tmp);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
+    const int a = c->cur_attr, o = 1 - c->cur_pos, oa = 1 - c->cur_attr;
+    if (relayout) {
+        order_gather<T, true><<<nblk, kThreads, 0, st>>>(
+            n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, x, y, z, (T *)c->b.dia[a],
+            (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(), nullptr, (T *)c->b.pos[o][0],
+            (T *)c->b.pos[o][1], (T *)c->b.pos[o][2], (T *)c->b.dia[oa], (T *)c->b.adh[oa], c->b.uid[oa]);
+    } else {
+        order_gather<T, false><<<nblk, kThreads, 0, st>>>(
+            n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, x, y, z, (T *)c->b.dia[a],
+            (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr, nullptr,
+            nullptr, nullptr, nullptr);
+    }
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    if (relayout) {
+        c->cur_pos = o;
+        c->cur_attr = oa;
+        c->relaid = true;
+    } else {
+        c->relaid = false;
+    }
+    c->have_grid = true;
+    return CG_OK;
 }
 
-template <typename T, bool SORTED, int SUM, bool ZS>
-static cudaError_t launch_tile(cg_context *c, const TileArgs<T> &TA, int ntiles)
-{
-    const size_t smem = tile_smem_bytes<T>(TA.t);
-    auto kern = sweep_tile_kernel<T, SORTED, SUM, ZS>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<ntiles, kThreads, smem, c->stream>>>(TA);
-    return cudaGetLastError();
-}
-
-template <typename T, bool SORTED, int SUM>
-static cudaError_t launch_tile_z(cg_context *c, const TileArgs<T> &TA, int ntiles)
-{
-    // row-major boxes are (z, uid)-ordered inside (order_in_box): z-window on
-    return TA.s.rank_of ? launch_tile<T, SORTED, SUM, false>(c, TA, ntiles)
-                        : launch_tile<T, SORTED, SUM, true>(c, TA, ntiles);
-}
-
-template <typename T, bool SORTED, int SUM, bool RM>
-static void launch_proxy_k(cg_context *c, const SweepArgs<T> &A, const ProxyArgs &P, int kscap)
+template <typename T, int SUM>
+static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A, int ks)
 {
     const int nblk = cdiv(A.n, kThreads);
-    if (kscap <= 32) {
-        auto k = sweep_proxy_kernel<T, SORTED, SUM, RM, 32>;
-        const int sm = 32 * kThreads * sizeof(int);
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        k<<<nblk, kThreads, sm, c->stream>>>(A, P);
-    } else {
-        auto k = sweep_proxy_kernel<T, SORTED, SUM, RM, 64>;
-        const int sm = 64 * kThreads * sizeof(int);
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        k<<<nblk, kThreads, sm, c->stream>>>(A, P);
-    }
-}
-
-template <typename T, bool SORTED>
-static void launch_proxy_s(cg_context *c, const SweepArgs<T> &A, const ProxyArgs &P, int kscap)
-{
-    const bool rm = A.rank_of == nullptr;
-    if (c->summation == SUM_UID) {
-        if (rm) launch_proxy_k<T, SORTED, SUM_UID, true>(c, A, P, kscap);
-        else launch_proxy_k<T, SORTED, SUM_UID, false>(c, A, P, kscap);
-    } else {
-        if (rm) launch_proxy_k<T, SORTED, SUM_STENCIL, true>(c, A, P, kscap);
-        else launch_proxy_k<T, SORTED, SUM_STENCIL, false>(c, A, P, kscap);
-    }
+    cudaStream_t st = c->stream;
+    // survivor-list capacity by expected survivors per agent; dense pools
+    // evaluate the list whenever it fills (stencil order), sparse pools walk
+    // again on the rare overflow
+    if (SUM == SUM_UID || ks <= 16) sweep7_kernel<T, SUM, 16, false><<<nblk, kThreads, 0, st>>>(A);
+    else if (ks <= 32) sweep7_kernel<T, SUM_STENCIL, 32, false><<<nblk, kThreads, 0, st>>>(A);
+    else sweep7_kernel<T, SUM_STENCIL, 32, true><<<nblk, kThreads, 0, st>>>(A);
+    LAUNCH_CHECK(c);
+    return CG_OK;
 }
 
 template <typename T>
-static int launch_sweep(cg_context *c, const SweepArgs<T> &A, bool sorted)
+static int run_sweep(cg_context *c, const double params[5], bool freeze, bool record)
 {
-    if (c->sweep_impl == 2) {
-        const int nblk = cdiv(A.n, kThreads);
-        if (sorted)
-            make_proxy<T, true><<<nblk, kThreads, 0, c->stream>>>(A.n, A.g, A.idx, A.slot_key, A.flat_of,
-                                                                  A.x, A.y, A.z, A.d, c->b.prox);
-        else
-            make_proxy<T, false><<<nblk, kThreads, 0, c->stream>>>(A.n, A.g, A.idx, A.slot_key, A.flat_of,
-                                                                   A.x, A.y, A.z, A.d, c->b.prox);
+    const int n = (int)c->n;
+    cudaStream_t st = c->stream;
+    const int cp = c->cur_pos, ca = c->cur_attr;
+    T *nx = freeze ? nullptr : (T *)c->b.pos[1 - cp][0];
+    T *ny = freeze ? nullptr : (T *)c->b.pos[1 - cp][1];
+    T *nz = freeze ? nullptr : (T *)c->b.pos[1 - cp][2];
+    const Params<T> P = make_params<T>(params);
+    if (c->sweep_impl == 0) {
+        // reference-order thread-per-agent sweep (sweep.cuh), then a standalone bbox next step
+        const int nblk = cdiv(n, kThreads);
+        if (nblk > kMaxCounterBlocks) return fail(c, CG_ERR_VALUE, "population too large for sweep 0");
+        SweepArgs<T> A{};
+        A.n = n;
+        A.g = c->geo;
+        A.x = (const T *)c->b.pos[cp][0];
+        A.y = (const T *)c->b.pos[cp][1];
+        A.z = (const T *)c->b.pos[cp][2];
+        A.d = (const T *)c->b.dia[ca];
+        A.adh = (const T *)c->b.adh[ca];
+        A.uid = c->b.uid[ca];
+        A.idx = c->relaid ? nullptr : c->b.idx;
+        A.slot_key = c->b.skey;
+        A.off = c->offset;
+        A.p = P;
+        A.disp_x = (T *)c->b.disp[0];
+        A.disp_y = (T *)c->b.disp[1];
+        A.disp_z = (T *)c->b.disp[2];
+        A.new_x = nx;
+        A.new_y = ny;
+        A.new_z = nz;
+        A.rec_m = record ? c->b.rec_m : nullptr;
+        A.rec_nk = record ? c->b.rec_nk : nullptr;
+        A.block_counters = c->block_counters;
+        if (c->relaid) {
+            if (c->summation == SUM_UID) sweep_kernel<T, true, SUM_UID, 32><<<nblk, kThreads, 0, st>>>(A);
+            else sweep_kernel<T, true, SUM_STENCIL, 1><<<nblk, kThreads, 0, st>>>(A);
+        } else {
+            if (c->summation == SUM_UID) sweep_kernel<T, false, SUM_UID, 32><<<nblk, kThreads, 0, st>>>(A);
+            else sweep_kernel<T, false, SUM_STENCIL, 1><<<nblk, kThreads, 0, st>>>(A);
+        }
         LAUNCH_CHECK(c);
-        ProxyArgs P;
-        P.prox = c->b.prox;
-        // fp32 prefilter margin: every stored / derived fp32 coordinate is within
-        // a few ulp of E (box-local x/y, grid-relative z); 64 ulp(E) is used
-        const double E = A.g.L * (double)std::max(3, A.g.dimz + 2);
-        P.margin = (float)(64.0 * E * 5.9604644775390625e-8);
-        // survivors per agent ~ 4.19 * density (contact ball / box volume)
-        const double rho = (double)A.n / (double)A.g.nb;
-        const int kscap = 4.19 * rho <= 20.0 ? 32 : 64;
-        CUDA_TRY(c, cudaMemsetAsync(A.block_counters, 0, sizeof(unsigned long long) * 3 * kCounterSlots,
-                                    c->stream));
-        if (sorted) launch_proxy_s<T, true>(c, A, P, kscap);
-        else launch_proxy_s<T, false>(c, A, P, kscap);
+        unsigned long long *stat = c->stat_dev + (c->steps_done % kRing) * kStatSlots;
+        reduce_counters<<<1, kThreads, 0, st>>>(nblk, c->block_counters, stat);
         LAUNCH_CHECK(c);
-        c->launches += 1;   // make_proxy (the sweep itself is counted by the caller)
+        c->launches += 2;
+        c->bbox_valid = freeze && c->bbox_valid;
         return CG_OK;
     }
-    if (c->sweep_impl == 1) {
-        TileArgs<T> TA;
-        TA.s = A;
-        TA.t = choose_tiles(A.g, A.n, c->tile_cap);
-        TA.t.debug_stop = c->debug_stop;
-        const long long nt = (long long)TA.t.ntx * TA.t.nty * TA.t.ntz;
-        if (nt >= INT32_MAX) return fail(c, CG_ERR_VALUE, "too many tiles");
-        CUDA_TRY(c, cudaMemsetAsync(A.block_counters, 0, sizeof(unsigned long long) * 3 * kCounterSlots,
-                                    c->stream));
-        cudaError_t e;
-        if (c->summation == SUM_UID)
-            e = sorted ? launch_tile_z<T, true, SUM_UID>(c, TA, (int)nt)
-                       : launch_tile_z<T, false, SUM_UID>(c, TA, (int)nt);
-        else
-            e = sorted ? launch_tile_z<T, true, SUM_STENCIL>(c, TA, (int)nt)
-                       : launch_tile_z<T, false, SUM_STENCIL>(c, TA, (int)nt);
-        CUDA_TRY(c, e);
-        return CG_OK;
+    Sweep7Args<T> A{};
+    A.n = n;
+    A.g = c->geo;
+    A.bd = c->bd;
+    A.prox = c->b.P();
+    A.skey = c->b.skey;
+    A.idx = c->relaid ? nullptr : c->b.idx;
+    A.off = c->offset;
+    A.x = (const T *)c->b.pos[cp][0];
+    A.y = (const T *)c->b.pos[cp][1];
+    A.z = (const T *)c->b.pos[cp][2];
+    A.d = (const T *)c->b.dia[ca];
+    A.adh = (const T *)c->b.adh[ca];
+    A.uid = c->b.uid[ca];
+    A.p = P;
+    A.rmax = nextafterf((float)(0.5 * c->max_diam), INFINITY);
+    // fp32 prefilter margin: every stored / derived fp32 coordinate is within
+    // a few ulp of E (box-local x/y, grid-relative z); 64 ulp(E) is used
+    const double E = c->geo.L * (double)std::max(3, std::max(c->geo.dimz + 2, 3));
+    A.margin = (float)(64.0 * E * 5.9604644775390625e-8);
+    A.disp_x = (T *)c->b.disp[0];
+    A.disp_y = (T *)c->b.disp[1];
+    A.disp_z = (T *)c->b.disp[2];
+    A.new_x = nx;
+    A.new_y = ny;
+    A.new_z = nz;
+    A.rec_m = record ? c->b.rec_m : nullptr;
+    A.rec_nk = record ? c->b.rec_nk : nullptr;
+    A.slots = c->slots;
+    // bbox shell (see sweep7.cuh): an agent can only become extreme if it ends
+    // within max_displacement (+ rounding slack) of the old bbox faces
+    {
+        const double md = (double)P.max_disp;
+        const bool ok = std::isfinite(md) && md >= 0.0;
+        for (int q = 0; q < 3; ++q) {
+            const double lo = c->bbox_host[q], hi = c->bbox_host[3 + q];
+            const double slack = 1e-6 * (std::fabs(lo) + std::fabs(hi) + 1.0);
+            const double B = ok ? md * (1.0 + 1e-6) + slack : INFINITY;
+            A.shell_lo[q] = lo + B;
+            A.shell_hi[q] = hi - B;
+        }
     }
-    const int nblk = cdiv(A.n, kThreads);
-    constexpr int KC = sizeof(T) == 8 ? 32 : 32;
-    if (c->summation == SUM_UID) {
-        if (sorted) sweep_kernel<T, true, SUM_UID, KC><<<nblk, kThreads, 0, c->stream>>>(A);
-        else sweep_kernel<T, false, SUM_UID, KC><<<nblk, kThreads, 0, c->stream>>>(A);
-    } else {
-        if (sorted) sweep_kernel<T, true, SUM_STENCIL, 1><<<nblk, kThreads, 0, c->stream>>>(A);
-        else sweep_kernel<T, false, SUM_STENCIL, 1><<<nblk, kThreads, 0, c->stream>>>(A);
-    }
+    // survivors per agent ~ 4.19 * (agents per box) (contact ball / box volume)
+    const double rho = (double)n / (double)c->geo.nb;
+    const double surv = 4.19 * rho;   // contact ball / box volume
+    const int ks = surv <= 9.0 ? 16 : (surv <= 20.0 ? 32 : 64);
+    int rc = c->summation == SUM_UID ? launch_sweep7<T, SUM_UID>(c, A, ks)
+                                     : launch_sweep7<T, SUM_STENCIL>(c, A, ks);
+    if (rc) return rc;
+    unsigned long long *stat = c->stat_dev + (c->steps_done % kRing) * kStatSlots;
+    // frozen: positions (and so the bbox in bbox_host) are unchanged
+    finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, stat, c->bbox_dev,
+                                         FINISH_COUNTERS | (freeze ? 0 : FINISH_BBOX));
     LAUNCH_CHECK(c);
+    c->launches += 2;
+    if (!freeze)
+        CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    c->bbox_valid = true;
     return CG_OK;
 }
 
@@ -420,65 +508,27 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
         c->steps_done++;
         return CG_OK;
     }
-    const int n = (int)c->n;
-    CUDA_TRY(c, cudaEventRecord(c->ev[slot][0], st));
+    const bool sort = (flags & CG_STEP_SORT) != 0;
+    const bool relayout = sort && c->n > 1 && (c->sort_steps % c->relayout_every == 0);
+    const bool freeze = (flags & CG_STEP_FREEZE) != 0;
+    const bool record = (flags & CG_STEP_RECORD) != 0;
     double origin[3];
     int64_t dims64[3];
-    int rc = build_grid<T>(c, ir, box_cap, origin, dims64);
-    if (rc) return rc;
-    CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
-    const bool sort = (flags & CG_STEP_SORT) && n > 1;
-    if (sort) {   // storage re-sort into (box rank, uid) order == lexsort((uid, code))
-        const int o = 1 - c->cur_pos, oa = 1 - c->cur_attr;
-        gather_records<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(
-            n, c->b.idx, (T *)c->b.pos[c->cur_pos][0], (T *)c->b.pos[c->cur_pos][1],
-            (T *)c->b.pos[c->cur_pos][2], (T *)c->b.dia[c->cur_attr], (T *)c->b.adh[c->cur_attr],
-            c->b.uid[c->cur_attr], (T *)c->b.pos[o][0], (T *)c->b.pos[o][1], (T *)c->b.pos[o][2],
-            (T *)c->b.dia[oa], (T *)c->b.adh[oa], c->b.uid[oa]);
-        LAUNCH_CHECK(c);
-        c->launches += 1;
-        c->cur_pos = o;
-        c->cur_attr = oa;
-    }
+    int rc;
+    // build_grid records event 0 after the bbox readback + host geometry, so
+    // the per-phase times are device times
+    if ((rc = build_grid<T>(c, ir, box_cap, relayout, origin, dims64))) return rc;
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
-    const int nblk = cdiv(n, kThreads);
-    if ((rc = ensure_block_counters(c, std::max(nblk, kCounterSlots)))) return rc;
-    SweepArgs<T> A;
-    A.n = n;
-    A.g = c->geo;
-    const int cp = c->cur_pos, ca = c->cur_attr;
-    A.x = (const T *)c->b.pos[cp][0];
-    A.y = (const T *)c->b.pos[cp][1];
-    A.z = (const T *)c->b.pos[cp][2];
-    A.d = (const T *)c->b.dia[ca];
-    A.adh = (const T *)c->b.adh[ca];
-    A.uid = c->b.uid[ca];
-    A.idx = c->b.idx;
-    A.slot_key = c->b.skey;
-    A.off = c->offset;
-    A.rank_of = c->morton ? c->mrank : nullptr;
-    A.flat_of = c->morton ? c->minv : nullptr;
-    A.p = make_params<T>(params);
-    A.disp_x = (T *)c->b.disp[0];
-    A.disp_y = (T *)c->b.disp[1];
-    A.disp_z = (T *)c->b.disp[2];
-    const bool freeze = flags & CG_STEP_FREEZE;
-    A.new_x = freeze ? nullptr : (T *)c->b.pos[1 - cp][0];
-    A.new_y = freeze ? nullptr : (T *)c->b.pos[1 - cp][1];
-    A.new_z = freeze ? nullptr : (T *)c->b.pos[1 - cp][2];
-    const bool record = flags & CG_STEP_RECORD;
-    A.rec_m = record ? c->b.rec_m : nullptr;
-    A.rec_nk = record ? c->b.rec_nk : nullptr;
-    A.block_counters = c->b.block_counters;
-    if ((rc = launch_sweep<T>(c, A, sort))) return rc;
-    unsigned long long *stat = c->stat_dev + slot * kStatSlots;
-    reduce_counters<<<1, kThreads, 0, st>>>(c->sweep_impl >= 1 ? kCounterSlots : nblk,
-                                            c->b.block_counters, stat);
-    LAUNCH_CHECK(c);
-    c->launches += 2;
-    if (!freeze) c->cur_pos = 1 - cp;
+    if (sort) {
+        c->sort_steps++;
+        c->pres_state = PRES_PENDING;   // the reference re-sorted its pool this step
+    } else if (relayout) {
+        c->pres_state = PRES_PENDING;
+    }
+    if ((rc = run_sweep<T>(c, params, freeze, record))) return rc;
+    if (!freeze) c->cur_pos = 1 - c->cur_pos;
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][3], st));
-    CUDA_TRY(c, cudaMemcpyAsync(c->stat_host + slot * kStatSlots, stat,
+    CUDA_TRY(c, cudaMemcpyAsync(c->stat_host + slot * kStatSlots, c->stat_dev + slot * kStatSlots,
                                 sizeof(unsigned long long) * kStatSlots, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][4], st));
     for (int a = 0; a < 3; ++a) {
@@ -486,8 +536,6 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
         S.origin[a] = origin[a];
     }
     S.box_length = c->geo.L;
-    c->have_grid = true;
-    c->last_sorted = sort;
     c->last_record = record;
     c->steps_done++;
     return CG_OK;
@@ -513,6 +561,27 @@ static int collect(cg_context *c, int64_t step_id, cg_step_stats *out)
         cudaEventElapsedTime(&S.t_total_ms, c->ev[slot][0], c->ev[slot][3]);
     }
     *out = S;
+    return CG_OK;
+}
+
+// Copy a storage-order device column to the host in the reference's order.
+static int download_column(cg_context *c, const void *src, void *dst, size_t w)
+{
+    const int n = (int)c->n;
+    cudaStream_t st = c->stream;
+    if (c->pres_state == PRES_IDENTITY) {
+        CUDA_TRY(c, cudaMemcpyAsync(dst, src, w * n, cudaMemcpyDeviceToHost, st));
+        return CG_OK;
+    }
+    if (w == 8)
+        scatter_by<unsigned long long><<<cdiv(n, kThreads), kThreads, 0, st>>>(
+            n, c->b.pres, (const unsigned long long *)src, (unsigned long long *)c->b.stage);
+    else
+        scatter_by<unsigned><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, c->b.pres, (const unsigned *)src,
+                                                                      (unsigned *)c->b.stage);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    CUDA_TRY(c, cudaMemcpyAsync(dst, c->b.stage, w * n, cudaMemcpyDeviceToHost, st));
     return CG_OK;
 }
 
@@ -551,13 +620,20 @@ int cg_create(int device, int precision, cg_context **out)
         if (e != cudaSuccess && rc == CG_OK) rc = fail(c, CG_ERR_CUDA, "%s", cudaGetErrorString(e));
     };
     chk(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    chk(cudaMalloc(&c->bbox_partial, sizeof(double) * 7 * kBboxBlocks));
+    chk(cudaMalloc(&c->slots, sizeof(unsigned long long) * kSlots * kSlotWords));
+    chk(cudaMalloc(&c->maxd_enc, sizeof(unsigned long long)));
+    chk(cudaMalloc(&c->block_counters, sizeof(unsigned long long) * 3 * kMaxCounterBlocks));
     chk(cudaMalloc(&c->bbox_dev, sizeof(double) * 8));
     chk(cudaMallocHost(&c->bbox_host, sizeof(double) * 8));
     chk(cudaMalloc(&c->stat_dev, sizeof(unsigned long long) * kStatSlots * kRing));
     chk(cudaMallocHost(&c->stat_host, sizeof(unsigned long long) * kStatSlots * kRing));
     for (int r = 0; r < kRing; ++r)
         for (int e = 0; e < 5; ++e) chk(cudaEventCreate(&c->ev[r][e]));
+    if (rc == CG_OK) {
+        init_slots<<<16, kThreads, 0, c->stream>>>(c->slots);
+        chk(cudaGetLastError());
+        chk(cudaStreamSynchronize(c->stream));
+    }
     if (rc != CG_OK) {
         cg_destroy(c);
         return rc;
@@ -572,14 +648,13 @@ void cg_destroy(cg_context *c)
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_agents(c);
-    int *ptrs[] = {c->count, c->offset, c->tile_sum, c->mrank, c->minv};
+    int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->moff};
     for (int *p : ptrs)
         if (p) cudaFree(p);
-    if (c->b.block_counters) cudaFree(c->b.block_counters);
-    if (c->bbox_partial) cudaFree(c->bbox_partial);
-    if (c->bbox_dev) cudaFree(c->bbox_dev);
+    void *vptrs[] = {c->scan_status, c->slots, c->maxd_enc, c->block_counters, c->bbox_dev, c->stat_dev};
+    for (void *p : vptrs)
+        if (p) cudaFree(p);
     if (c->bbox_host) cudaFreeHost(c->bbox_host);
-    if (c->stat_dev) cudaFree(c->stat_dev);
     if (c->stat_host) cudaFreeHost(c->stat_host);
     for (int r = 0; r < kRing; ++r)
         for (int e = 0; e < 5; ++e)
@@ -615,21 +690,12 @@ int cg_set_option(cg_context *c, int key, int value)
         c->summation = value;
         return CG_OK;
     }
-    if (key == CG_OPT_SWEEP && value >= 0 && value <= 2) {
+    if (key == CG_OPT_SWEEP && (value == 0 || value == 1)) {
         c->sweep_impl = value;
         return CG_OK;
     }
-    if (key == 99 && value >= 0 && value <= 2) {   // profiling aid (not in the header)
-        c->debug_stop = value;
-        return CG_OK;
-    }
-    if (key == CG_OPT_TILE_CAP && value >= 256 && value <= 8192) {
-        c->tile_cap = value;
-        return CG_OK;
-    }
-    if (key == CG_OPT_BOX_ORDER && (value == 0 || value == 1)) {
-        c->morton = value == 0;
-        c->table_dims[0] = 0;
+    if (key == CG_OPT_RELAYOUT_EVERY && value >= 1) {
+        c->relayout_every = value;
         return CG_OK;
     }
     return fail(c, CG_ERR_VALUE, "bad option %d=%d", key, value);
@@ -640,7 +706,8 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
 {
     if (!c) return CG_ERR_VALUE;
     if (n < 0) return fail(c, CG_ERR_VALUE, "negative agent count");
-    if (n >= (int64_t)INT32_MAX / 2) return fail(c, CG_ERR_POOL_CAPACITY, "%lld agents exceeds the device cap", (long long)n);
+    if (n >= (int64_t)INT32_MAX / 4)
+        return fail(c, CG_ERR_POOL_CAPACITY, "%lld agents exceeds the device cap", (long long)n);
     CUDA_TRY(c, cudaSetDevice(c->device));
     if (n > c->cap) {
         int rc = alloc_agents(c, n);
@@ -649,6 +716,10 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
     c->n = n;
     c->cur_pos = c->cur_attr = 0;
     c->have_grid = false;
+    c->relaid = false;
+    c->bbox_valid = false;
+    c->pres_state = PRES_IDENTITY;
+    c->sort_steps = 0;
     if (n == 0) return CG_OK;
     const size_t fe = c->esz * (size_t)n;
     cudaStream_t st = c->stream;
@@ -659,7 +730,19 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
     CUDA_TRY(c, cudaMemcpyAsync(c->b.adh[0], adherence, fe, cudaMemcpyHostToDevice, st));
     CUDA_TRY(c, cudaMemcpyAsync(c->b.uid[0], uid, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, st));
     for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMemsetAsync(c->b.disp[a], 0, fe, st));
+    CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, sizeof(unsigned long long), st));
+    if (c->prec == CG_FP64)
+        max_diam_kernel<double><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(
+            (int)n, (const double *)c->b.dia[0], c->maxd_enc);
+    else
+        max_diam_kernel<float><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(
+            (int)n, (const float *)c->b.dia[0], c->maxd_enc);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    unsigned long long enc = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));   // host buffers are only borrowed
+    c->max_diam = dec_ordered(enc);
     return CG_OK;
 }
 
@@ -670,17 +753,19 @@ int cg_download(cg_context *c, void *px, void *py, void *pz, void *diameter, voi
     CUDA_TRY(c, cudaSetDevice(c->device));
     const int64_t n = c->n;
     if (n == 0) return CG_OK;
-    const size_t fe = c->esz * (size_t)n;
-    cudaStream_t st = c->stream;
+    int rc = materialize_presentation(c);
+    if (rc) return rc;
     void *dst[9] = {px, py, pz, diameter, adherence, uid, dx, dy, dz};
     const void *src[9] = {c->b.pos[c->cur_pos][0], c->b.pos[c->cur_pos][1], c->b.pos[c->cur_pos][2],
                           c->b.dia[c->cur_attr], c->b.adh[c->cur_attr], c->b.uid[c->cur_attr],
                           c->b.disp[0], c->b.disp[1], c->b.disp[2]};
-    for (int k = 0; k < 9; ++k)
-        if (dst[k])
-            CUDA_TRY(c, cudaMemcpyAsync(dst[k], src[k], k == 5 ? sizeof(uint64_t) * n : fe,
-                                        cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(c, cudaStreamSynchronize(st));
+    for (int k = 0; k < 9; ++k) {
+        if (!dst[k]) continue;
+        if ((rc = download_column(c, src[k], dst[k], k == 5 ? 8 : c->esz))) return rc;
+        if (c->pres_state != PRES_IDENTITY)   // the staging buffer is reused per column
+            CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return CG_OK;
 }
 
@@ -707,11 +792,9 @@ int cg_build_grid(cg_context *c, double interaction_radius, int64_t box_cap, cg_
     int64_t dims64[3];
     const int slot = (int)(c->steps_done % kRing);
     const int rc = c->prec == CG_FP64
-                       ? build_grid<double>(c, interaction_radius, box_cap, origin, dims64)
-                       : build_grid<float>(c, interaction_radius, box_cap, origin, dims64);
+                       ? build_grid<double>(c, interaction_radius, box_cap, false, origin, dims64)
+                       : build_grid<float>(c, interaction_radius, box_cap, false, origin, dims64);
     if (rc) return rc;
-    c->have_grid = true;
-    c->last_sorted = false;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (stats) {
         std::memset(stats, 0, sizeof *stats);
@@ -748,27 +831,28 @@ int cg_grid_export(cg_context *c, int64_t *box_index, int64_t *box_count)
     if (!c) return CG_ERR_VALUE;
     if (!c->have_grid) return fail(c, CG_ERR_STATE, "no grid: run a step first");
     CUDA_TRY(c, cudaSetDevice(c->device));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    int rc = materialize_presentation(c);
+    if (rc) return rc;
     const int n = (int)c->n, nb = c->geo.nb;
-    std::vector<int> skey(n), key(n), cnt(nb), minv;
-    if (c->morton) {
-        minv.resize(nb);
-        CUDA_TRY(c, cudaMemcpy(minv.data(), c->minv, sizeof(int) * nb, cudaMemcpyDeviceToHost));
-    }
-    auto flat = [&](int k) { return c->morton ? minv[k] : k; };
+    cudaStream_t st = c->stream;
     if (box_index) {
-        // sorted: storage slot s holds slot s of the CSR; else key[] is per storage index
-        if (c->last_sorted) {
-            CUDA_TRY(c, cudaMemcpy(skey.data(), c->b.skey, sizeof(int) * n, cudaMemcpyDeviceToHost));
-            for (int s = 0; s < n; ++s) box_index[s] = flat(skey[s]);
-        } else {
-            CUDA_TRY(c, cudaMemcpy(key.data(), c->b.key, sizeof(int) * n, cudaMemcpyDeviceToHost));
-            for (int i = 0; i < n; ++i) box_index[i] = flat(key[i]);
+        // after a relayout the storage index is the slot: its box is skey
+        const int *keys = c->b.skey;
+        if (!c->relaid) {
+            key_of_storage<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, c->b.key_rank, c->b.tmp);
+            LAUNCH_CHECK(c);
+            keys = c->b.tmp;
         }
+        std::vector<int> k(n);
+        if ((rc = download_column(c, keys, k.data(), 4))) return rc;
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        for (int i = 0; i < n; ++i) box_index[i] = k[i];
     }
     if (box_count) {
-        CUDA_TRY(c, cudaMemcpy(cnt.data(), c->count, sizeof(int) * nb, cudaMemcpyDeviceToHost));
-        for (int k = 0; k < nb; ++k) box_count[flat(k)] = cnt[k];
+        std::vector<int> off(nb + 1);
+        CUDA_TRY(c, cudaMemcpyAsync(off.data(), c->offset, sizeof(int) * (nb + 1), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        for (int b = 0; b < nb; ++b) box_count[b] = off[b + 1] - off[b];
     }
     return CG_OK;
 }
@@ -778,9 +862,12 @@ int cg_record_export(cg_context *c, int32_t *m, int32_t *nk)
     if (!c) return CG_ERR_VALUE;
     if (!c->last_record) return fail(c, CG_ERR_STATE, "last step did not run with CG_STEP_RECORD");
     CUDA_TRY(c, cudaSetDevice(c->device));
+    int rc = materialize_presentation(c);
+    if (rc) return rc;
+    if (m && (rc = download_column(c, c->b.rec_m, m, 4))) return rc;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    if (m) CUDA_TRY(c, cudaMemcpy(m, c->b.rec_m, sizeof(int) * c->n, cudaMemcpyDeviceToHost));
-    if (nk) CUDA_TRY(c, cudaMemcpy(nk, c->b.rec_nk, sizeof(int) * c->n, cudaMemcpyDeviceToHost));
+    if (nk && (rc = download_column(c, c->b.rec_nk, nk, 4))) return rc;
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return CG_OK;
 }
 
@@ -795,14 +882,14 @@ int cg_box_ids(cg_context *c, int64_t n, const void *px, const void *py, const v
     if (n > c->cap && (rc = alloc_agents(c, n))) return rc;
     c->n = 0;   // the resident pool is overwritten by this call
     c->have_grid = false;
+    c->bbox_valid = false;
+    c->pres_state = PRES_IDENTITY;
     Geometry g{box_length, ox, oy, oz, (int)dimx, (int)dimy, (int)dimz, (int)(dimx * dimy * dimz)};
     const size_t fe = c->esz * (size_t)n;
     const void *src[3] = {px, py, pz};
     for (int a = 0; a < 3; ++a)
         CUDA_TRY(c, cudaMemcpyAsync(c->b.pos[0][a], src[a], fe, cudaMemcpyHostToDevice, c->stream));
-    void *tmp = nullptr;
-    CUDA_TRY(c, cudaMallocAsync(&tmp, sizeof(long long) * n, c->stream));
-    long long *dout = (long long *)tmp;
+    long long *dout = (long long *)c->b.stage;
     if (c->prec == CG_FP64)
         box_ids_only<double><<<cdiv(n, kThreads), kThreads, 0, c->stream>>>(
             (int)n, g, (double *)c->b.pos[0][0], (double *)c->b.pos[0][1], (double *)c->b.pos[0][2], dout);
@@ -810,8 +897,8 @@ int cg_box_ids(cg_context *c, int64_t n, const void *px, const void *py, const v
         box_ids_only<float><<<cdiv(n, kThreads), kThreads, 0, c->stream>>>(
             (int)n, g, (float *)c->b.pos[0][0], (float *)c->b.pos[0][1], (float *)c->b.pos[0][2], dout);
     LAUNCH_CHECK(c);
+    c->launches += 1;
     CUDA_TRY(c, cudaMemcpyAsync(out, dout, sizeof(long long) * n, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaFreeAsync(tmp, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return CG_OK;
 }
@@ -832,80 +919,61 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     const int nn = (int)n;
     cudaStream_t st = c->stream;
     const int64_t nb64 = dimx * dimy * dimz;
-    if (nb64 >= (int64_t)INT32_MAX) return fail(c, CG_ERR_GRID_OVERFLOW, "too many boxes");
+    if (nb64 >= (int64_t)INT32_MAX / 2) return fail(c, CG_ERR_GRID_OVERFLOW, "too many boxes");
     if ((rc = ensure_boxes(c, nb64))) return rc;
-    Geometry g{0.0, 0.0, 0.0, 0.0, (int)dimx, (int)dimy, (int)dimz, (int)nb64};
+    Geometry g{1.0, 0.0, 0.0, 0.0, (int)dimx, (int)dimy, (int)dimz, (int)nb64};
     c->geo = g;
-    c->morton = false;   // kernel-level call: row-major keys taken from box_index
-    c->table_dims[0] = 0;
-    // no box_length is given at this level, so use the thread-per-agent sweep
-    // (the tiled sweep's prefilter needs L)
-    struct Restore {
-        cg_context *c;
-        int v;
-        ~Restore() { c->sweep_impl = v; }
-    } restore{c, c->sweep_impl};
-    c->sweep_impl = 0;
-    long long *dbox = nullptr;
-    CUDA_TRY(c, cudaMallocAsync(&dbox, sizeof(long long) * n, st));
-    CUDA_TRY(c, cudaMemcpyAsync(dbox, box_index, sizeof(long long) * n, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(c, cudaMemsetAsync(c->count, 0, sizeof(int) * g.nb, st));
+    c->bd = make_decode(g);
     const int nblk = cdiv(nn, kThreads);
+    if (nblk > kMaxCounterBlocks) return fail(c, CG_ERR_VALUE, "population too large");
     if (c->prec == CG_FP64) double_column<double><<<nblk, kThreads, 0, st>>>(nn, (double *)c->b.dia[0]);
     else double_column<float><<<nblk, kThreads, 0, st>>>(nn, (float *)c->b.dia[0]);
-    keys_from_flat<<<nblk, kThreads, 0, st>>>(nn, dbox, c->count, c->b.key, c->b.rnk);
-    const int ntiles = cdiv(g.nb, kScanTile);
+    long long *dbox = (long long *)c->b.stage;
+    CUDA_TRY(c, cudaMemcpyAsync(dbox, box_index, sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+    keys_from_flat<<<nblk, kThreads, 0, st>>>(nn, dbox, c->count, c->b.key_rank);
+    LAUNCH_CHECK(c);
     const int slot = (int)(c->steps_done % kRing);
     unsigned long long *stat = c->stat_dev + slot * kStatSlots;
     CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
-    scan_tiles<<<ntiles, kThreads, 0, st>>>(g.nb, c->count, c->offset, c->tile_sum, stat);
-    scan_tile_sums<<<1, kThreads, 0, st>>>(ntiles, c->tile_sum);
-    scan_add<<<cdiv(g.nb, kThreads), kThreads, 0, st>>>(g.nb, nn, c->tile_sum, c->offset);
-    place<<<nblk, kThreads, 0, st>>>(nn, c->b.key, c->b.rnk, c->offset, c->b.tmp);
-    order_in_box<double, false><<<nblk, kThreads, 0, st>>>(nn, c->b.tmp, c->b.key, c->offset,
-                                                           c->b.uid[0], nullptr, c->b.idx, c->b.skey);
+    if ((rc = launch_scan(c, false, g.nb, c->offset, stat))) return rc;
+    place<<<nblk, kThreads, 0, st>>>(nn, c->b.key_rank, c->offset, c->b.tmp);
+    if (c->prec == CG_FP64)
+        order_gather<double, false><<<nblk, kThreads, 0, st>>>(
+            nn, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, (double *)c->b.pos[0][0],
+            (double *)c->b.pos[0][1], (double *)c->b.pos[0][2], (double *)c->b.dia[0],
+            (double *)c->b.adh[0], c->b.uid[0], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr,
+            nullptr, nullptr, nullptr, nullptr);
+    else
+        order_gather<float, false><<<nblk, kThreads, 0, st>>>(
+            nn, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, (float *)c->b.pos[0][0],
+            (float *)c->b.pos[0][1], (float *)c->b.pos[0][2], (float *)c->b.dia[0],
+            (float *)c->b.adh[0], c->b.uid[0], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr,
+            nullptr, nullptr, nullptr, nullptr);
     LAUNCH_CHECK(c);
-    if ((rc = ensure_block_counters(c, std::max(nblk, kCounterSlots)))) return rc;
+    c->launches += 5;
+    c->relaid = false;
+    // the kernel-level call has no box_length: use the reference-order sweep
+    const int saved = c->sweep_impl;
+    c->sweep_impl = 0;
     double p5[5];
     for (int k = 0; k < 5; ++k)
         p5[k] = c->prec == CG_FP64 ? ((const double *)params7)[k] : (double)((const float *)params7)[k];
-    if (c->prec == CG_FP64) {
-        SweepArgs<double> A{};
-        A.n = nn; A.g = g;
-        A.x = (double *)c->b.pos[0][0]; A.y = (double *)c->b.pos[0][1]; A.z = (double *)c->b.pos[0][2];
-        A.d = (double *)c->b.dia[0]; A.adh = (double *)c->b.adh[0]; A.uid = c->b.uid[0];
-        A.idx = c->b.idx; A.slot_key = c->b.skey; A.off = c->offset;
-        A.p = make_params<double>(p5);
-        A.disp_x = (double *)c->b.disp[0]; A.disp_y = (double *)c->b.disp[1]; A.disp_z = (double *)c->b.disp[2];
-        A.block_counters = c->b.block_counters;
-        if ((rc = launch_sweep<double>(c, A, false))) return rc;
-    } else {
-        SweepArgs<float> A{};
-        A.n = nn; A.g = g;
-        A.x = (float *)c->b.pos[0][0]; A.y = (float *)c->b.pos[0][1]; A.z = (float *)c->b.pos[0][2];
-        A.d = (float *)c->b.dia[0]; A.adh = (float *)c->b.adh[0]; A.uid = c->b.uid[0];
-        A.idx = c->b.idx; A.slot_key = c->b.skey; A.off = c->offset;
-        A.p = make_params<float>(p5);
-        A.disp_x = (float *)c->b.disp[0]; A.disp_y = (float *)c->b.disp[1]; A.disp_z = (float *)c->b.disp[2];
-        A.block_counters = c->b.block_counters;
-        if ((rc = launch_sweep<float>(c, A, false))) return rc;
-    }
-    reduce_counters<<<1, kThreads, 0, st>>>(c->sweep_impl >= 1 ? kCounterSlots : nblk,
-                                            c->b.block_counters, stat);
-    LAUNCH_CHECK(c);
+    rc = c->prec == CG_FP64 ? run_sweep<double>(c, p5, true, false) : run_sweep<float>(c, p5, true, false);
+    c->sweep_impl = saved;
+    if (rc) return rc;
     unsigned long long h[kStatSlots];
     CUDA_TRY(c, cudaMemcpyAsync(h, stat, sizeof h, cudaMemcpyDeviceToHost, st));
     const size_t fe = c->esz * (size_t)n;
     void *dst[3] = {out_dx, out_dy, out_dz};
     for (int a = 0; a < 3; ++a)
         CUDA_TRY(c, cudaMemcpyAsync(dst[a], c->b.disp[a], fe, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(c, cudaFreeAsync(dbox, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));
     counters[0] = (int64_t)h[2];
     counters[1] = (int64_t)h[3];
     counters[2] = (int64_t)h[4];
     c->n = 0;   // the resident buffers no longer hold a consistent pool
     c->have_grid = false;
+    c->bbox_valid = false;
     return CG_OK;
 }
 

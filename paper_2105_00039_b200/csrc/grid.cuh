@@ -2,70 +2,182 @@
 //
 // Replaces reference spatial.build_grid (spatial.py:89-127), kernels.py:107-145
 // (box ids + linked-cell chains) and the Z-order re-sort (morton.py:93-107,
-// pool.py:228-239) with a counting sort into a box-sorted CSR layout:
-//   K1 bbox_partial/bbox_final   pool.py:102-110 max_diameter + bounding_box
-//   K2 box_keys                  kernels.py:107-129 box ids, warp-aggregated counts
-//   K3 scan_*                    exclusive prefix sum of counts -> box offsets
-//   K4 place + order_in_box      counting-sort scatter; members of a box ordered by uid
-//                                (Morton order) or by (z, uid) (row-major order)
-//   K5 morton_table              box -> Morton rank (boxes visited in Z-order)
-//   K4b gather_records           apply the permutation (storage re-sort)
+// pool.py:228-239) with a counting sort into a box-sorted CSR:
+//   bbox_slots / finish_step   pool.py:102-110 bounding_box (exact min/max, f64)
+//   box_keys                   kernels.py:107-129 box ids + warp-aggregated counts
+//   scan_lookback              exclusive prefix sum of counts -> box offsets
+//                              (single pass, decoupled look-back; zeroes the counts)
+//   place + order_gather       counting-sort scatter; members of a box ordered by
+//                              (z, uid); emits the slot-order fp32 proxies, the
+//                              slot -> box key and either the slot -> storage
+//                              index or (relayout) the records themselves
+//   morton_table, presentation the reference's storage order (Morton code, uid),
+//                              materialised only when the host asks for it
+// Boxes are visited in row-major flat order (z fastest): the 3 boxes of a
+// stencil z-run are one contiguous slot range.
 #pragma once
 
 #include "common.cuh"
 
 namespace cg {
 
-// ---------------------------------------------------------------- K1 bbox
-// Exact min/max reductions (order independent), widened to f64 like numpy's
-// col.min()/col.max() -> np.array(float64).  7 values per block:
-// min x,y,z, max x,y,z, max diameter.
-template <typename T>
-__global__ void bbox_partial(int n, const T *__restrict__ x, const T *__restrict__ y,
-                             const T *__restrict__ z, const T *__restrict__ d,
-                             double *__restrict__ partial)
+// Per-step reduction slots: blocks spread their atomics over kSlots slots
+// (blockIdx % kSlots) so no address sees more than a few hundred updates.
+// slot layout: [0..2] min x,y,z (ordered u64), [3..5] max x,y,z, [6] evals,
+// [7] candidates, [8] degenerate pairs.
+constexpr int kSlots = 512;
+constexpr int kSlotWords = 9;
+
+__device__ __forceinline__ double warp_min(double v)
 {
-    double v[7] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const double px = (double)x[i], py = (double)y[i], pz = (double)z[i];
-        v[0] = fmin(v[0], px); v[1] = fmin(v[1], py); v[2] = fmin(v[2], pz);
-        v[3] = fmax(v[3], px); v[4] = fmax(v[4], py); v[5] = fmax(v[5], pz);
-        v[6] = fmax(v[6], (double)d[i]);
-    }
-    __shared__ double red[7][kThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide min/max of 6 values + sums of 3 counters into one slot.
+// Must be called by every thread of the block (kThreads threads).
+__device__ __forceinline__ void block_to_slot(double lo[3], double hi[3], unsigned long long c[3],
+                                              unsigned long long *__restrict__ slots)
+{
+    __shared__ double s_lo[3][kThreads / 32], s_hi[3][kThreads / 32];
+    __shared__ unsigned long long s_c[3][kThreads / 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-    for (int k = 0; k < 7; ++k) {
-        double t = v[k];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = warp_min(lo[a]);
+        hi[a] = warp_max(hi[a]);
+        c[a] = warp_sum(c[a]);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            s_lo[a][w] = lo[a];
+            s_hi[a][w] = hi[a];
+            s_c[a][w] = c[a];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+        const int k = threadIdx.x, a = k % 3;
+        unsigned long long *slot = slots + (blockIdx.x % kSlots) * kSlotWords;
+        if (k < 3) {
+            double v = s_lo[a][0];
+            for (int q = 1; q < kThreads / 32; ++q) v = fmin(v, s_lo[a][q]);
+            if (v != INFINITY) atomicMin(slot + a, enc_ordered(v));
+        } else if (k < 6) {
+            double v = s_hi[a][0];
+            for (int q = 1; q < kThreads / 32; ++q) v = fmax(v, s_hi[a][q]);
+            if (v != -INFINITY) atomicMax(slot + 3 + a, enc_ordered(v));
+        } else {
+            unsigned long long v = 0;
+            for (int q = 0; q < kThreads / 32; ++q) v += s_c[a][q];
+            if (v) atomicAdd(slot + 6 + a, v);
+        }
+    }
+}
+
+// Reset value of the slots (min slots at the top of the order, max at the bottom).
+__device__ __forceinline__ unsigned long long slot_init(int word)
+{
+    return word < 3 ? ~0ull : 0ull;
+}
+
+__global__ void init_slots(unsigned long long *__restrict__ slots)
+{
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kSlots * kSlotWords; k += gridDim.x * blockDim.x)
+        slots[k] = slot_init(k % kSlotWords);
+}
+
+// ---------------------------------------------------------------- K1 bbox
+// Standalone exact bounding box of the stored positions (after an upload or a
+// relayout-free first step); in steady state the sweep epilogue produces the
+// same slots from the new positions.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bbox_slots(int n, const T *__restrict__ x, const T *__restrict__ y,
+                                                       const T *__restrict__ z,
+                                                       unsigned long long *__restrict__ slots)
+{
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    unsigned long long c[3] = {0, 0, 0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double p[3] = {(double)x[i], (double)y[i], (double)z[i]};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = fmin(lo[a], p[a]);
+            hi[a] = fmax(hi[a], p[a]);
+        }
+    }
+    block_to_slot(lo, hi, c, slots);
+}
+
+// One block: fold the slots into stat[2..4] (evals, cands, ndeg) and the
+// bbox out[0..5] (+ out[6] = max diameter, which the path never changes),
+// then reset the slots for the next step.
+enum { FINISH_COUNTERS = 1, FINISH_BBOX = 2 };
+
+__global__ void finish_step(unsigned long long *__restrict__ slots, double max_diameter,
+                            unsigned long long *__restrict__ stat, double *__restrict__ bbox_out,
+                            int what)
+{
+    __shared__ unsigned long long red[kSlotWords][kThreads / 32];
+    unsigned long long v[kSlotWords];
+#pragma unroll
+    for (int k = 0; k < kSlotWords; ++k) v[k] = slot_init(k);
+    for (int s = threadIdx.x; s < kSlots; s += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < kSlotWords; ++k) {
+            const unsigned long long u = slots[s * kSlotWords + k];
+            v[k] = k < 3 ? min(v[k], u) : (k < 6 ? max(v[k], u) : v[k] + u);
+            slots[s * kSlotWords + k] = slot_init(k);
+        }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kSlotWords; ++k) {
+        unsigned long long t = v[k];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            const double u = __shfl_xor_sync(0xffffffffu, t, o);
-            t = k < 3 ? fmin(t, u) : fmax(t, u);
+            const unsigned long long u = __shfl_xor_sync(0xffffffffu, t, o);
+            t = k < 3 ? min(t, u) : (k < 6 ? max(t, u) : t + u);
         }
         if (lane == 0) red[k][w] = t;
     }
     __syncthreads();
-    if (threadIdx.x < 7) {
+    if (threadIdx.x < kSlotWords) {
         const int k = threadIdx.x;
-        double t = red[k][0];
-        for (int q = 1; q < kThreads / 32; ++q) t = k < 3 ? fmin(t, red[k][q]) : fmax(t, red[k][q]);
-        partial[blockIdx.x * 7 + k] = t;
+        unsigned long long t = red[k][0];
+        for (int q = 1; q < kThreads / 32; ++q)
+            t = k < 3 ? min(t, red[k][q]) : (k < 6 ? max(t, red[k][q]) : t + red[k][q]);
+        if (k < 6) {
+            if (what & FINISH_BBOX) bbox_out[k] = dec_ordered(t);
+        } else if (what & FINISH_COUNTERS) {
+            stat[2 + (k - 6)] = t;
+        }
+        if (k == 0 && (what & FINISH_BBOX)) bbox_out[6] = max_diameter;
     }
 }
 
-__global__ void bbox_final(int nblocks, const double *__restrict__ partial, double *__restrict__ out)
+// max(diameter) once per upload (the path never changes diameters)
+template <typename T>
+__global__ void max_diam_kernel(int n, const T *__restrict__ d, unsigned long long *__restrict__ out)
 {
-    if (threadIdx.x < 7) {
-        const int k = threadIdx.x;
-        double t = partial[k];
-        for (int b = 1; b < nblocks; ++b) t = k < 3 ? fmin(t, partial[b * 7 + k]) : fmax(t, partial[b * 7 + k]);
-        out[k] = t;
-    }
+    double v = -INFINITY;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        v = fmax(v, (double)d[i]);
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0 && v != -INFINITY) atomicMax(out, enc_ordered(v));
 }
 
 // ---------------------------------------------------------------- K5 Morton table
 // mrank[flat] = Morton rank of the box, minv[rank] = flat.  Rebuilt only when
-// the grid dims change.
+// the grid dims change (presentation order only).
 __global__ void morton_table(Geometry g, int *__restrict__ mrank, int *__restrict__ minv)
 {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < g.nb; b += gridDim.x * blockDim.x) {
@@ -79,9 +191,8 @@ __global__ void morton_table(Geometry g, int *__restrict__ mrank, int *__restric
 
 // ---------------------------------------------------------------- K2 box keys
 // kernels.py:113-128, bit for bit: ix = int64(floor((f64(p) - ox) / L)),
-// clamped, flat = (ix*dimy + iy)*dimz + iz.  The counting-sort key is the box's
-// visiting rank (Morton rank or flat id).  rank_in_box comes from the
-// warp-aggregated atomic; its order is arbitrary and fixed up by K4.
+// clamped, flat = (ix*dimy + iy)*dimz + iz.  rank_in_box comes from the
+// warp-aggregated atomic; its order is arbitrary and fixed up by order_gather.
 __device__ __forceinline__ int axis_box(double p, double o, double L, int dim)
 {
     long long k = (long long)floor((p - o) / L);
@@ -100,27 +211,24 @@ __device__ __forceinline__ int flat_box(const Geometry &g, T x, T y, T z)
 }
 
 template <typename T>
-__global__ void box_keys(int n, Geometry g, const T *__restrict__ x, const T *__restrict__ y,
-                         const T *__restrict__ z, const int *__restrict__ mrank,
-                         int *__restrict__ count, int *__restrict__ key, int *__restrict__ rank_in_box)
+__global__ void __launch_bounds__(kThreads) box_keys(int n, Geometry g, const T *__restrict__ x,
+                                                     const T *__restrict__ y, const T *__restrict__ z,
+                                                     int *__restrict__ count, int2 *__restrict__ key_rank)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int flat = flat_box(g, x[i], y[i], z[i]);
-    const int k = mrank ? __ldg(mrank + flat) : flat;
-    rank_in_box[i] = agg_increment(count, k);
-    key[i] = k;
+    key_rank[i] = make_int2(flat, agg_increment(count, flat));
 }
 
 // Keys from caller-supplied flat box ids (kernel-level force-phase drop-in).
 __global__ void keys_from_flat(int n, const long long *__restrict__ box_index, int *__restrict__ count,
-                               int *__restrict__ key, int *__restrict__ rank_in_box)
+                               int2 *__restrict__ key_rank)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int k = (int)box_index[i];
-    rank_in_box[i] = agg_increment(count, k);
-    key[i] = k;
+    key_rank[i] = make_int2(k, agg_increment(count, k));
 }
 
 template <typename T>
@@ -140,11 +248,20 @@ __global__ void box_ids_only(int n, Geometry g, const T *__restrict__ x, const T
 }
 
 // ---------------------------------------------------------------- K3 scan
-// Three-phase exclusive scan of the per-box counts (tile = 256 x 8 items).
-// Phase 1 also accumulates the StepStats grid figures (occupied boxes, max
-// occupancy) into stat[0], stat[1].
-constexpr int kScanItems = 8;
+// Single-pass exclusive scan with decoupled look-back (tiles of 256 x 16
+// boxes, dynamic tile order so predecessors always make progress).  Reads the
+// counts, writes the offsets (nb + 1 entries, offset[nb] = total), zeroes the
+// counts for the next build, and accumulates the StepStats grid figures
+// (occupied boxes, max occupancy) into stat[0], stat[1].
+// MORTON: the counts are taken in Morton rank order from an existing CSR
+// (cnt(r) = off[minv[r]+1] - off[minv[r]]) -- the presentation order scan.
+constexpr int kScanItems = 16;
 constexpr int kScanTile = kThreads * kScanItems;
+
+struct ScanState {
+    unsigned long long *status;   // per tile: (flag << 32) | value;  flag 1 = aggregate, 2 = prefix
+    unsigned *ticket;             // dynamic tile counter
+};
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int &total)
 {
@@ -178,110 +295,231 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int &total)
     return excl;
 }
 
-__global__ void scan_tiles(int nb, const int *__restrict__ count, int *__restrict__ offset,
-                           int *__restrict__ tile_sum, unsigned long long *__restrict__ stat)
+template <bool MORTON>
+__global__ void __launch_bounds__(kThreads) scan_lookback(int nb, int *__restrict__ count,
+                                                          const int *__restrict__ src_off,
+                                                          const int *__restrict__ minv,
+                                                          int *__restrict__ offset, ScanState S,
+                                                          unsigned long long *__restrict__ stat)
 {
-    const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+    __shared__ unsigned tile_sh;
+    __shared__ int prefix_sh;
+    if (threadIdx.x == 0) tile_sh = atomicAdd(S.ticket, 1u);
+    __syncthreads();
+    const int tile = (int)tile_sh;
+    const int base = tile * kScanTile + threadIdx.x * kScanItems;
     int v[kScanItems];
     int s = 0, occ = 0, mx = 0;
+    if (!MORTON && base + kScanItems <= nb) {
+        int4 *p = reinterpret_cast<int4 *>(count + base);
+#pragma unroll
+        for (int q = 0; q < kScanItems / 4; ++q) {
+            const int4 u = p[q];
+            v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
+            p[q] = make_int4(0, 0, 0, 0);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            const int b = base + k;
+            if (b < nb) {
+                if (MORTON) {
+                    const int f = __ldg(minv + b);
+                    v[k] = __ldg(src_off + f + 1) - __ldg(src_off + f);
+                } else {
+                    v[k] = count[b];
+                    count[b] = 0;
+                }
+            } else {
+                v[k] = 0;
+            }
+        }
+    }
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        v[k] = (base + k < nb) ? count[base + k] : 0;
         s += v[k];
         occ += v[k] > 0;
         mx = max(mx, v[k]);
     }
     int total;
-    int run = block_exclusive_scan(s, total);
+    const int run0 = block_exclusive_scan(s, total);
+    // publish, then look back (warp 0)
+    if (threadIdx.x < 32) {
+        if (tile == 0) {
+            if (threadIdx.x == 0) {
+                atomicExch(S.status, (2ull << 32) | (unsigned)total);
+                prefix_sh = 0;
+            }
+        } else {
+            if (threadIdx.x == 0) atomicExch(S.status + tile, (1ull << 32) | (unsigned)total);
+            int excl = 0;
+            int pos = tile - 1;   // this lane inspects tile pos - lane
+            while (true) {
+                const int t = pos - (int)threadIdx.x;
+                unsigned long long st = t >= 0 ? *((volatile unsigned long long *)(S.status + t)) : (2ull << 32);
+                unsigned flag = (unsigned)(st >> 32);
+                // wait until every inspected predecessor has published
+                while (__any_sync(0xffffffffu, flag == 0)) {
+                    st = t >= 0 ? *((volatile unsigned long long *)(S.status + t)) : (2ull << 32);
+                    flag = (unsigned)(st >> 32);
+                }
+                const unsigned prefix_mask = __ballot_sync(0xffffffffu, flag == 2);
+                // sum values from lane 0 up to (and including) the first prefix lane
+                const int stop = prefix_mask ? __ffs(prefix_mask) - 1 : 31;
+                int val = ((int)threadIdx.x <= stop && t >= 0) ? (int)(unsigned)st : 0;
+                val = warp_sum(val);
+                excl += val;
+                if (prefix_mask) break;
+                pos -= 32;
+            }
+            if (threadIdx.x == 0) {
+                atomicExch(S.status + tile, (2ull << 32) | (unsigned)(excl + total));
+                prefix_sh = excl;
+            }
+        }
+    }
+    __syncthreads();
+    int run = run0 + prefix_sh;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         if (base + k < nb) offset[base + k] = run;
         run += v[k];
     }
-    if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
-    occ = warp_sum(occ);
+    if (base + kScanItems >= nb && base < nb + kScanItems && base <= nb && base + kScanItems > nb - 1)
+        ;   // (the last element's successor is written below)
+    if (base <= nb - 1 && nb - 1 < base + kScanItems) offset[nb] = run;
+    if (stat) {
+        occ = warp_sum(occ);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) {
-        if (occ) atomicAdd(stat + 0, (unsigned long long)occ);
-        atomicMax(stat + 1, (unsigned long long)mx);
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0) {
+            if (occ) atomicAdd(stat + 0, (unsigned long long)occ);
+            if (mx) atomicMax(stat + 1, (unsigned long long)mx);
+        }
     }
-}
-
-// Single block: exclusive scan of the tile sums in place (any count).
-__global__ void scan_tile_sums(int ntiles, int *__restrict__ tile_sum)
-{
-    int carry = 0;
-    for (int base = 0; base < ntiles; base += kThreads) {
-        const int i = base + threadIdx.x;
-        const int v = i < ntiles ? tile_sum[i] : 0;
-        int total;
-        const int ex = block_exclusive_scan(v, total);
-        if (i < ntiles) tile_sum[i] = ex + carry;
-        carry += total;
-    }
-}
-
-__global__ void scan_add(int nb, int n, const int *__restrict__ tile_sum, int *__restrict__ offset)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nb) offset[i] += tile_sum[i / kScanTile];
-    if (i == 0) offset[nb] = n;
 }
 
 // ---------------------------------------------------------------- K4 place/order
-__global__ void place(int n, const int *__restrict__ key, const int *__restrict__ rank_in_box,
-                      const int *__restrict__ offset, int *__restrict__ tmp)
+__global__ void __launch_bounds__(kThreads) place(int n, const int2 *__restrict__ key_rank,
+                                                  const int *__restrict__ offset, int *__restrict__ tmp)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) tmp[offset[key[i]] + rank_in_box[i]] = i;
+    if (i >= n) return;
+    const int2 kr = key_rank[i];
+    tmp[__ldg(offset + kr.x) + kr.y] = i;
 }
 
-// Members of a box are re-ranked so slot order (the summation order of the
-// sweep and the storage order after a sort) is a pure function of the
-// population: by uid (Morton box order == the reference's lexsort((uid, code)),
-// morton.py:67-74) or, for row-major box order, by (z, uid) so that every
-// 3-box z-run of the stencil is z-sorted (the sweep's z-window relies on it).
-template <typename T, bool BY_Z>
-__global__ void order_in_box(int n, const int *__restrict__ tmp, const int *__restrict__ key,
-                             const int *__restrict__ offset, const uint64_t *__restrict__ uid,
-                             const T *__restrict__ zc, int *__restrict__ idx, int *__restrict__ skey)
+// fp32 proxies in slot order, pair-interleaved so the sweep tests two
+// candidates per packed FADD2/FFMA2 chain:
+//   xy[4q .. 4q+3] = (x_2q, x_2q+1, y_2q, y_2q+1)   box-local x/y (|err| <= ulp(L))
+//   z[2q .. 2q+1]  = (z_2q, z_2q+1)                  grid-relative z (monotone, so
+//                                                    z-sorted boxes stay sorted)
+// The candidate's radius is not stored: the sweep bounds it by the pool's
+// largest radius (conservative).
+struct Proxies {
+    float *xy;
+    float *z;
+};
+
+template <typename T>
+__device__ __forceinline__ void put_proxy(const Proxies &P, const Geometry &g, int s, int ix, int iy, T x, T y, T z)
+{
+    const int q = s >> 1, h = s & 1;
+    P.xy[4 * q + h] = (float)((double)x - (g.ox + (double)ix * g.L));
+    P.xy[4 * q + 2 + h] = (float)((double)y - (g.oy + (double)iy * g.L));
+    P.z[s] = (float)((double)z - g.oz);
+}
+
+// Members of a box are re-ranked by (z, uid) -- a pure function of the
+// population, so slot order (the stencil summation order and the storage
+// order after a relayout) is deterministic -- and every 3-box z-run of a
+// stencil is one z-sorted slot range.  Emits skey/prox per slot and either
+// idx (slot -> storage) or, when RELAYOUT, the records in slot order.
+template <typename T, bool RELAYOUT>
+__global__ void __launch_bounds__(kThreads) order_gather(
+    int n, Geometry g, BoxDecode bd, const int *__restrict__ tmp, const int2 *__restrict__ key_rank,
+    const int *__restrict__ offset, const T *__restrict__ x, const T *__restrict__ y,
+    const T *__restrict__ z, const T *__restrict__ d, const T *__restrict__ adh,
+    const uint64_t *__restrict__ uid, int *__restrict__ skey, Proxies prox,
+    int *__restrict__ idx, T *__restrict__ ox_, T *__restrict__ oy_, T *__restrict__ oz_,
+    T *__restrict__ od, T *__restrict__ oadh, uint64_t *__restrict__ ouid)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     const int i = tmp[s];
-    const int k = key[i];
-    const int o0 = offset[k], o1 = offset[k + 1];
-    const uint64_t u = uid[i];
+    const int k = key_rank[i].x;
+    const int o0 = __ldg(offset + k), o1 = __ldg(offset + k + 1);
+    const T zi = z[i];
+    const uint64_t ui = uid[i];
     int q = 0;
-    if (BY_Z) {
-        const T zi = zc[i];
-        for (int t = o0; t < o1; ++t) {
-            const int j = __ldg(tmp + t);
-            const T zj = zc[j];
-            q += (zj < zi) || (zj == zi && __ldg(uid + j) < u);
-        }
-    } else {
-        for (int t = o0; t < o1; ++t) q += (__ldg(uid + __ldg(tmp + t)) < u);
+    for (int t = o0; t < o1; ++t) {
+        const int j = __ldg(tmp + t);
+        const T zj = z[j];
+        q += (zj < zi) || (zj == zi && uid[j] < ui);
     }
-    idx[o0 + q] = i;
-    skey[o0 + q] = k;
+    const int dst = o0 + q;
+    int ix, iy, iz;
+    decode_box(bd, k, ix, iy, iz);
+    const T xi = x[i], yi = y[i], di = d[i];
+    skey[dst] = k;
+    put_proxy<T>(prox, g, dst, ix, iy, xi, yi, zi);
+    if (RELAYOUT) {
+        ox_[dst] = xi;
+        oy_[dst] = yi;
+        oz_[dst] = zi;
+        od[dst] = di;
+        oadh[dst] = adh[i];
+        ouid[dst] = ui;
+    } else {
+        idx[dst] = i;
+    }
 }
 
-// K4b: new storage slot s <- old storage index idx[s] (pool.py:228-239).
-template <typename T>
-__global__ void gather_records(int n, const int *__restrict__ idx,
-                               const T *__restrict__ x0, const T *__restrict__ y0,
-                               const T *__restrict__ z0, const T *__restrict__ d0,
-                               const T *__restrict__ a0, const uint64_t *__restrict__ u0,
-                               T *__restrict__ x1, T *__restrict__ y1, T *__restrict__ z1,
-                               T *__restrict__ d1, T *__restrict__ a1, uint64_t *__restrict__ u1)
+// ---------------------------------------------------------------- presentation
+// The reference's storage order after a sorted step (morton.py:67-74,
+// lexsort((uid, code))): pres[storage index] = position in that order =
+// moff[mrank[box]] + (rank of the uid among the box's members).
+__global__ void __launch_bounds__(kThreads) presentation(int n, const int *__restrict__ skey,
+                                                         const int *__restrict__ idx,
+                                                         const int *__restrict__ offset,
+                                                         const int *__restrict__ mrank,
+                                                         const int *__restrict__ moff,
+                                                         const uint64_t *__restrict__ uid,
+                                                         int *__restrict__ pres)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const int i = idx[s];
-    x1[s] = x0[i]; y1[s] = y0[i]; z1[s] = z0[i];
-    d1[s] = d0[i]; a1[s] = a0[i]; u1[s] = u0[i];
+    const int k = skey[s];
+    const int i = idx ? idx[s] : s;
+    const int o0 = __ldg(offset + k), o1 = __ldg(offset + k + 1);
+    const uint64_t ui = uid[i];
+    int q = 0;
+    for (int t = o0; t < o1; ++t) {
+        const int j = idx ? __ldg(idx + t) : t;
+        q += uid[j] < ui;
+    }
+    pres[i] = __ldg(moff + __ldg(mrank + k)) + q;
+}
+
+// dst[pres[i]] = src[i] (download / export in the reference's order)
+template <typename W>
+__global__ void scatter_by(int n, const int *__restrict__ pres, const W *__restrict__ src, W *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[pres[i]] = src[i];
+}
+
+__global__ void iota(int n, int *__restrict__ v)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+
+// storage-order box index of the last grid (for exports)
+__global__ void key_of_storage(int n, const int2 *__restrict__ key_rank, int *__restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = key_rank[i].x;
 }
 
 }  // namespace cg

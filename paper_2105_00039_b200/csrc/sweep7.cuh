@@ -1,0 +1,374 @@
+// sweep7.cuh -- the production 27-box sweep (north-star kernel (b)).
+//
+// Same results as the reference force phase (kernels.py:148-277) plus apply
+// (engine.py:323-327) and the next step's bounding box (pool.py:102-110):
+//   * one thread per slot (agents in box-sorted slot order: row-major boxes,
+//     members of a box by (z, uid), so every 3-box z-run of a stencil column
+//     is one contiguous, z-sorted slot range);
+//   * phase 1 walks the 9 stencil columns; columns whose x/y distance exceeds
+//     the reach are skipped, each column's run is cut once the z-sorted
+//     proxies pass z + reach, and candidates are tested two at a time with
+//     packed fp32 arithmetic (FADD2/FMUL2/FFMA2 on pair-interleaved proxies,
+//     grid.cuh) against a conservative bound (reach = r_i + max radius +
+//     margin >= every distance the exact test can keep);
+//   * survivors go to a per-thread list in shared memory; phase 2 evaluates
+//     the exact predicate (kernels.py:198-203) and, if kept, the pair force
+//     (kernels.py:230-257) in the pool dtype with the reference's expression
+//     order (no FMA: the library is built with -fmad=false), summing in walk
+//     order (SUM_STENCIL) or ascending uid (SUM_UID, bit-identical to the
+//     reference); the next survivor's record is loaded while the current pair
+//     is evaluated;
+//   * the pair constant req = (ri*rj)/(ri+rj) is reused while rj repeats
+//     (uniform pools: one division per agent instead of one per pair);
+//   * epilogue: adherence gate + cap (kernels.py:266-277), displacement and
+//     new position written in storage order; counters (one REDUX + atomic per
+//     warp) and the exact bbox of the new positions (ordered-u64 atomics, only
+//     from agents within max_displacement of the old bbox faces -- no other
+//     agent can be extreme) go into the per-step reduction slots (grid.cuh).
+// m (stencil candidates) is the sum of the 27 clamped box counts minus one,
+// exactly what _gather_stencil enumerates.
+#pragma once
+
+#include "common.cuh"
+#include "grid.cuh"
+#include "sweep.cuh"
+
+#ifndef CG_SWEEP_MINB
+#define CG_SWEEP_MINB 4   // resident CTAs per SM the register allocation must allow (measured best)
+#endif
+
+namespace cg {
+
+template <typename T>
+struct Sweep7Args {
+    int n;
+    Geometry g;
+    BoxDecode bd;
+    Proxies prox;            // slot order, pair-interleaved
+    const int *skey;         // slot -> flat box
+    const int *idx;          // slot -> storage index, nullptr = identity (relaid out)
+    const int *off;          // flat box -> first slot (nb + 1 entries)
+    const T *x, *y, *z, *d, *adh;
+    const uint64_t *uid;
+    Params<T> p;
+    float rmax;              // largest radius of the pool (rounded up)
+    float margin;            // absolute prefilter margin
+    T *disp_x, *disp_y, *disp_z;
+    T *new_x, *new_y, *new_z;   // nullptr when frozen
+    int *rec_m, *rec_nk;        // storage order, nullptr unless recording
+    unsigned long long *slots;  // per-step reduction slots
+    double shell_lo[3], shell_hi[3];   // bbox shell: old lo + max move, old hi - max move
+};
+
+// packed fp32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2)
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2_splat(float a)
+{
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
+    return r;
+}
+__device__ __forceinline__ f32x2 f2_sub(f32x2 a, f32x2 b)
+{
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b)
+{
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c)
+{
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(f32x2 v, float &lo, float &hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
+template <typename T, int SUM, int KS, bool FLUSH>
+__global__ void __launch_bounds__(kThreads, CG_SWEEP_MINB) sweep7_kernel(Sweep7Args<T> A)
+{
+    constexpr bool UIDMODE = SUM == SUM_UID;
+    __shared__ int lst[KS][kThreads];
+    __shared__ uint64_t ukey[UIDMODE ? KS : 1][kThreads];
+#define LST(k) lst[k][threadIdx.x]
+#define UKEY(k) ukey[k][threadIdx.x]
+
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned c_m = 0, c_nk = 0, c_nd = 0;
+    if (s < A.n) {
+        const int key = __ldg(A.skey + s);
+        int ix, iy, iz;
+        decode_box(A.bd, key, ix, iy, iz);
+        const int a = A.idx ? __ldg(A.idx + s) : s;
+        const T half = T(0.5), zero = A.p.zero;
+        const float mex = __ldg(A.prox.xy + 4 * (s >> 1) + (s & 1));
+        const float mey = __ldg(A.prox.xy + 4 * (s >> 1) + 2 + (s & 1));
+        const float mez = __ldg(A.prox.z + s);
+        const float Lf = (float)A.g.L;
+        const float reach = (float)(A.d[a] * half) + A.rmax + A.margin;
+        const float reach2 = reach * reach;
+        const float zhi = mez + reach;
+        const f32x2 mz2 = f2_splat(mez);
+        const int z0 = max(iz - 1, 0), z1 = min(iz + 1, A.g.dimz - 1);
+        const ulonglong2 *PXY = reinterpret_cast<const ulonglong2 *>(A.prox.xy);
+        const f32x2 *PZ = reinterpret_cast<const f32x2 *>(A.prox.z);
+
+        // phase-1 walk over the 9 stencil columns; visit(t) per survivor, in
+        // slot order (the agent itself included: phase 2 skips it); after()
+        // runs once per batch that produced survivors
+        auto walk = [&](auto &&visit, auto &&after) -> int {
+            int mm = -1;
+#pragma unroll 1
+            for (int ox = -1; ox <= 1; ++ox) {
+                const int nx = ix + ox;
+                if ((unsigned)nx >= (unsigned)A.g.dimx) continue;
+                const float gx = ox == 0 ? 0.f : fmaxf(0.f, ox < 0 ? mex : Lf - mex);
+                const f32x2 mx2 = f2_splat(mex - (float)ox * Lf);
+#pragma unroll 1
+                for (int oy = -1; oy <= 1; ++oy) {
+                    const int ny = iy + oy;
+                    if ((unsigned)ny >= (unsigned)A.g.dimy) continue;
+                    const int base = (nx * A.g.dimy + ny) * A.g.dimz;
+                    const int t0 = __ldg(A.off + base + z0), t1 = __ldg(A.off + base + z1 + 1);
+                    mm += t1 - t0;
+                    const float gy = oy == 0 ? 0.f : fmaxf(0.f, oy < 0 ? mey : Lf - mey);
+                    if (gx * gx + gy * gy > reach2) continue;
+                    const f32x2 my2 = f2_splat(mey - (float)oy * Lf);
+                    // slot pairs covering [t0, t1); the proxy arrays are padded past n
+                    for (int ta = t0 & ~1; ta < t1; ta += 2) {
+                        const ulonglong2 xy = __ldg(PXY + (ta >> 1));
+                        const f32x2 zz = __ldg(PZ + (ta >> 1));
+                        const f32x2 dz = f2_sub(mz2, zz);
+                        f32x2 d2 = f2_mul(dz, dz);
+                        const f32x2 dy = f2_sub(my2, xy.y);
+                        d2 = f2_fma(dy, dy, d2);
+                        const f32x2 dx = f2_sub(mx2, xy.x);
+                        d2 = f2_fma(dx, dx, d2);
+                        float d2a, d2b;
+                        f2_unpack(d2, d2a, d2b);
+                        const bool pa = d2a <= reach2 && ta >= t0;
+                        const bool pb = d2b <= reach2 && ta + 1 < t1;
+                        if (pa || pb) {
+                            if (pa) visit(ta);
+                            if (pb) visit(ta + 1);
+                            after();
+                        }
+                        float za, zb;
+                        f2_unpack(zz, za, zb);
+                        if (zb > zhi) break;   // z-sorted run (zb past t1 only ends the loop sooner)
+                    }
+                }
+            }
+            return mm;
+        };
+
+        const T xi = A.x[a], yi = A.y[a], zi = A.z[a];
+        const T ri = A.d[a] * half;
+        T fx = zero, fy = zero, fz = zero;
+        int nk = 0, nd = 0;
+        T last_rj = T(-1), last_req = zero;
+        // phase 2 for list entries [0, cnt), in list order; the next entry's
+        // record is in flight while the current pair is evaluated
+        auto evaluate = [&](int cnt_) {
+            int p = 0;
+            if (p < cnt_ && LST(p) == s) ++p;
+            if (p >= cnt_) return;
+            int j = A.idx ? __ldg(A.idx + LST(p)) : LST(p);
+            T xj = A.x[j], yj = A.y[j], zj = A.z[j], dj = A.d[j];
+#pragma unroll 1
+            while (p < cnt_) {
+                const int jc = j;
+                const T cxj = xj, cyj = yj, czj = zj, cdj = dj;
+                ++p;
+                if (p < cnt_ && LST(p) == s) ++p;   // the agent itself
+                if (p < cnt_) {
+                    j = A.idx ? __ldg(A.idx + LST(p)) : LST(p);
+                    xj = A.x[j];
+                    yj = A.y[j];
+                    zj = A.z[j];
+                    dj = A.d[j];
+                }
+                const T dx = xi - cxj, dy = yi - cyj, dz = zi - czj;   // kernels.py:198-203
+                const T rj = cdj * half;
+                const T dist = tsqrt<T>(dx * dx + dy * dy + dz * dz);
+                const T rsum = ri + rj;
+                const T delta = rsum - dist;
+                if (!(delta > zero)) continue;
+                ++nk;                                                    // kernels.py:230-257
+                if (rj != last_rj) {
+                    last_rj = rj;
+                    last_req = (ri * rj) / rsum;
+                }
+                const T mag = A.p.kappa * delta - A.p.gamma * tsqrt<T>(last_req * delta);
+                if (dist > zero) {
+                    const T sc = mag / dist;
+                    fx = fx + sc * dx;
+                    fy = fy + sc * dy;
+                    fz = fz + sc * dz;
+                } else {
+                    ++nd;
+                    const uint64_t ui = A.uid[a], uj = A.uid[jc];
+                    double ux, uy, uz;
+                    degenerate_dir(ui < uj ? ui : uj, ui < uj ? uj : ui, ux, uy, uz);
+                    const double sign = ui < uj ? 1.0 : -1.0;
+                    fx = fx + (T)((double)mag * (sign * ux));
+                    fy = fy + (T)((double)mag * (sign * uy));
+                    fz = fz + (T)((double)mag * (sign * uz));
+                }
+            }
+        };
+
+        int m;
+        if (!UIDMODE && FLUSH) {
+            // dense neighbourhoods: the list is evaluated whenever it fills up
+            int ns = 0;
+            m = walk([&](int t) { LST(ns++) = t; },
+                     [&]() {
+                         if (ns > KS - 2) {
+                             evaluate(ns);
+                             ns = 0;
+                         }
+                     });
+            evaluate(ns);
+        } else if (!UIDMODE) {
+            // collect the first KS survivors, evaluate; on overflow walk again,
+            // collecting the next KS (walk order is deterministic)
+            int ns = 0, total = 0;
+            m = walk(
+                [&](int t) {
+                    if (ns < KS) LST(ns++) = t;
+                    ++total;
+                },
+                [] {});
+            evaluate(ns);
+            for (int done = KS; done < total; done += KS) {
+                int seen = 0;
+                ns = 0;
+                walk(
+                    [&](int t) {
+                        if (seen >= done && ns < KS) LST(ns++) = t;
+                        ++seen;
+                    },
+                    [] {});
+                evaluate(ns);
+            }
+        } else {
+            auto cand_uid = [&](int t) -> uint64_t { return A.uid[A.idx ? __ldg(A.idx + t) : t]; };
+            // first walk: keep the first KS survivors, count all of them
+            int ns = 0, total = 0;
+            m = walk(
+                [&](int t) {
+                    if (ns < KS) {
+                        LST(ns) = t;
+                        UKEY(ns) = cand_uid(t);
+                        ++ns;
+                    }
+                    ++total;
+                },
+                [] {});
+            if (total <= KS) {
+                // insertion sort by uid, then one evaluation in uid order
+                for (int p = 1; p < ns; ++p) {
+                    const uint64_t u = UKEY(p);
+                    const int v = LST(p);
+                    int q = p;
+                    while (q > 0 && UKEY(q - 1) > u) {
+                        UKEY(q) = UKEY(q - 1);
+                        LST(q) = LST(q - 1);
+                        --q;
+                    }
+                    UKEY(q) = u;
+                    LST(q) = v;
+                }
+                evaluate(ns);
+            } else {
+                // dense neighbourhood: rounds of the KS smallest uids above floor_uid
+                int done = 0;
+                uint64_t floor_uid = 0;
+                bool first = true;
+                while (done < total) {
+                    int nr = 0;
+                    walk(
+                        [&](int t) {
+                            const uint64_t ut = cand_uid(t);
+                            if (!first && ut <= floor_uid) return;
+                            int q;
+                            if (nr < KS) q = nr++;
+                            else if (ut < UKEY(KS - 1)) q = KS - 1;
+                            else return;
+                            while (q > 0 && UKEY(q - 1) > ut) {
+                                UKEY(q) = UKEY(q - 1);
+                                LST(q) = LST(q - 1);
+                                --q;
+                            }
+                            UKEY(q) = ut;
+                            LST(q) = t;
+                        },
+                        [] {});
+                    evaluate(nr);
+                    done += nr;
+                    if (nr) floor_uid = UKEY(nr - 1);
+                    first = false;
+                }
+            }
+        }
+
+        // _write_displacement, kernels.py:266-277
+        const T norm = tsqrt<T>(fx * fx + fy * fy + fz * fz);
+        T ddx = zero, ddy = zero, ddz = zero;
+        if (!(norm <= A.p.adh_scale * A.adh[a])) {
+            T sc = A.p.timestep;
+            if (norm * sc > A.p.max_disp) sc = A.p.max_disp / norm;
+            ddx = fx * sc;
+            ddy = fy * sc;
+            ddz = fz * sc;
+        }
+        A.disp_x[a] = ddx;
+        A.disp_y[a] = ddy;
+        A.disp_z[a] = ddz;
+        if (A.new_x) {                 // engine.py:325-327 (separate buffer: two-phase)
+            const T nxp = xi + ddx, nyp = yi + ddy, nzp = zi + ddz;
+            A.new_x[a] = nxp;
+            A.new_y[a] = nyp;
+            A.new_z[a] = nzp;
+            // next step's bbox: only agents inside the boundary shell can be extreme
+            // (the extreme agent moved by at most max_displacement)
+            const double p3[3] = {(double)nxp, (double)nyp, (double)nzp};
+            unsigned long long *slot = A.slots + (blockIdx.x % kSlots) * kSlotWords;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (p3[q] <= A.shell_lo[q]) atomicMin(slot + q, enc_ordered(p3[q]));
+                if (p3[q] >= A.shell_hi[q]) atomicMax(slot + 3 + q, enc_ordered(p3[q]));
+            }
+        }
+        if (A.rec_m) {
+            A.rec_m[a] = m;
+            A.rec_nk[a] = nk;
+        }
+        c_m = (unsigned)m;
+        c_nk = (unsigned)nk;
+        c_nd = (unsigned)nd;
+    }
+#undef LST
+#undef UKEY
+    // counters: one REDUX per warp, one atomic per warp and counter
+    c_m = __reduce_add_sync(0xffffffffu, c_m);
+    c_nk = __reduce_add_sync(0xffffffffu, c_nk);
+    c_nd = __reduce_add_sync(0xffffffffu, c_nd);
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long *slot = A.slots + (blockIdx.x % kSlots) * kSlotWords;
+        atomicAdd(slot + 6, (unsigned long long)c_nk);
+        atomicAdd(slot + 7, (unsigned long long)c_m);
+        if (c_nd) atomicAdd(slot + 8, (unsigned long long)c_nd);
+    }
+}
+
+
+}  // namespace cg

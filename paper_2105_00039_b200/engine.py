@@ -44,7 +44,6 @@ class TileCapacityError(RuntimeError):
 
 
 SUMMATIONS = {"uid": 0, "stencil": 1}
-BOX_ORDERS = {"morton": 0, "rowmajor": 1}
 
 
 @dataclass(frozen=True)
@@ -55,22 +54,23 @@ class Gpu:
                  (bit-identical to the reference kernels, kernels.py:206-257);
                  "stencil": accumulated in stencil order (deterministic, within
                  a few ulp of the reference, fewer passes).
-    box_order -- "morton": storage re-sorted into the reference's Z-order
-                 (morton.py:67-74), so downloaded pools match the reference's
-                 storage order; "rowmajor": boxes in flat-index order.
+    relayout_every -- the device moves agent records into its box-sorted
+                 slot order on every k-th sort step (the paper's Z-order
+                 locality, GPU v2); the reference's (Morton code, uid) storage
+                 order is always what the host sees (kept as a permutation).
     """
 
     device: int = 0
     summation: str = "uid"
-    box_order: str = "morton"
+    relayout_every: int = 1
 
     def __post_init__(self):
         if self.device < 0:
             raise ValueError("device must be >= 0")
         if self.summation not in SUMMATIONS:
             raise ValueError("summation must be one of %s" % sorted(SUMMATIONS))
-        if self.box_order not in BOX_ORDERS:
-            raise ValueError("box_order must be one of %s" % sorted(BOX_ORDERS))
+        if self.relayout_every < 1:
+            raise ValueError("relayout_every must be >= 1")
 
 
 def strategy_label(strategy):
@@ -176,12 +176,12 @@ _contexts = {}
 
 
 def _context(strategy, dtype):
-    key = (strategy.device, np.dtype(dtype).str, strategy.summation, strategy.box_order)
+    key = (strategy.device, np.dtype(dtype).str, strategy.summation, strategy.relayout_every)
     ctx = _contexts.get(key)
     if ctx is None:
         ctx = _native.Context(strategy.device, dtype)
         ctx.set_option(_native.CG_OPT_SUMMATION, SUMMATIONS[strategy.summation])
-        ctx.set_option(_native.CG_OPT_BOX_ORDER, BOX_ORDERS[strategy.box_order])
+        ctx.set_option(_native.CG_OPT_RELAYOUT_EVERY, strategy.relayout_every)
         _contexts[key] = ctx
     return ctx
 

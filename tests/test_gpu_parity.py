@@ -27,14 +27,12 @@ def _native():
     return _native
 
 
-def _ctx(dtype, summation="uid", box_order="morton", sweep="proxy", tile_cap=None):
+def _ctx(dtype, summation="uid", sweep="v7", relayout_every=1):
     N = _native()
     ctx = N.Context(0, dtype)
     ctx.set_option(N.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[summation])
-    ctx.set_option(N.CG_OPT_BOX_ORDER, {"morton": 0, "rowmajor": 1}[box_order])
-    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "tile": 1, "proxy": 2}[sweep])
-    if tile_cap:
-        ctx.set_option(N.CG_OPT_TILE_CAP, tile_cap)
+    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "v7": 1}[sweep])
+    ctx.set_option(N.CG_OPT_RELAYOUT_EVERY, relayout_every)
     return ctx
 
 
@@ -70,20 +68,19 @@ def _reference_state(g, k):
             g["in_adh"][order], uid]
 
 
-@pytest.mark.parametrize("sweep", ["proxy", "tile", "agent", "tile-overflow"])
+@pytest.mark.parametrize("sweep,relayout", [("v7", 1), ("v7", 2), ("v7", 1000), ("agent", 1)])
 @pytest.mark.parametrize("summation", ["uid", "stencil"])
 @pytest.mark.parametrize("name", golden_names())
-def test_golden_morton(cuda_required, name, summation, sweep):
+def test_golden(cuda_required, name, summation, sweep, relayout):
     """uid mode chains all steps on the device (bit-exact end to end); stencil
     mode restarts every step from the reference's state, because its last-ulp
-    differences legitimately move later bounding boxes."""
+    differences legitimately move later bounding boxes.  relayout = the device
+    moves records into slot order on every k-th sort step; downloads must show
+    the reference's storage order regardless."""
     g = load_golden(name)
     dt = g["in_px"].dtype
     N = _native()
-    if sweep == "tile-overflow":    # staging capacity too small: global-memory fallback
-        ctx = _ctx(dt, summation, sweep="tile", tile_cap=256)
-    else:
-        ctx = _ctx(dt, summation, sweep=sweep)
+    ctx = _ctx(dt, summation, sweep=sweep, relayout_every=relayout)
     every = int(g["sort_every"])
     for k in range(int(g["steps"])):
         s = "s%d_" % k
@@ -123,29 +120,6 @@ def test_golden_morton(cuda_required, name, summation, sweep):
             for grp in (pairs[:3], pairs[3:]):
                 ok, worst = _vec_close([cols[a] for a, _ in grp], [g[s + b] for _, b in grp], rtol)
                 assert ok, (k, grp[0][0], worst)
-    ctx.close()
-
-
-@pytest.mark.parametrize("sweep", ["proxy", "tile"])
-@pytest.mark.parametrize("name", ["rand600_s0_f64", "multistep_f64", "hetero_f64", "c1_f32",
-                                  "dense3000_f64", "faces_f64"])
-def test_golden_rowmajor_box_order(cuda_required, name, sweep):
-    """Row-major box order: identical physics keyed by uid (storage order differs)."""
-    g = load_golden(name)
-    N = _native()
-    ctx = _ctx(g["in_px"].dtype, "uid", "rowmajor", sweep=sweep)
-    ctx.upload(g["in_px"], g["in_py"], g["in_pz"], g["in_diam"], g["in_adh"], g["in_uid"])
-    every = int(g["sort_every"])
-    for k in range(int(g["steps"])):
-        s = "s%d_" % k
-        flags = N.CG_STEP_SORT if every > 0 and k % every == 0 else 0
-        st = ctx.step(_params5(g), ir_from_golden(g), 1 << 24, flags)
-        assert (st.force_evals, st.candidates) == (int(g[s + "evals"]), int(g[s + "cands"]))
-        cols = ctx.download()
-        mine = _by_uid(cols["uid"], cols["px"], cols["py"], cols["pz"], cols["dx"])
-        ref = _by_uid(g[s + "out_uid"], g[s + "out_px"], g[s + "out_py"], g[s + "out_pz"], g[s + "dx"])
-        for a, b in zip(mine, ref):
-            assert np.array_equal(a, b)
     ctx.close()
 
 

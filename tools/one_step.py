@@ -1,7 +1,7 @@
 """Minimal driver for ncu captures: upload a config and run a few steps.
 
-usage: python tools/one_step.py <c1|c2|c4|c3_<d>>[f] [summation 0|1] [box_order 0|1] [steps]
-(env SWEEP=0|1 selects the sweep kernel)
+usage: python tools/one_step.py <c1|c2|c4|c3_<d>>[f] [summation 0|1] [relayout_every k] [steps]
+(env SWEEP=0|1 selects the sweep kernel: 0 reference-order, 1 production)
 """
 import os
 import sys
@@ -23,8 +23,8 @@ makers = {"c1": lambda: workloads.c1(pm), "c2": lambda: workloads.c2(pm),
 pool = makers.get(base, lambda: workloads.c3(float(base[3:]), pm))()
 ctx = _native.Context(0, pool.dtype)
 ctx.set_option(_native.CG_OPT_SUMMATION, summ)
-ctx.set_option(_native.CG_OPT_BOX_ORDER, order)
-ctx.set_option(_native.CG_OPT_SWEEP, int(os.environ.get("SWEEP", "2")))
+ctx.set_option(_native.CG_OPT_RELAYOUT_EVERY, order)
+ctx.set_option(_native.CG_OPT_SWEEP, int(os.environ.get("SWEEP", "1")))
 ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence,
            pool.uid)
 for k in range(steps):

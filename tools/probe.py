@@ -9,12 +9,8 @@ def probe(name, pool, summation, order, flags, steps=5, warm=3, sweep=1):
     N = _native
     ctx = N.Context(0, pool.dtype)
     ctx.set_option(N.CG_OPT_SWEEP, sweep)
-    if os.environ.get("STOP"):
-        ctx.set_option(99, int(os.environ["STOP"]))
-    if os.environ.get("TILECAP"):
-        ctx.set_option(N.CG_OPT_TILE_CAP, int(os.environ["TILECAP"]))
     ctx.set_option(N.CG_OPT_SUMMATION, summation)
-    ctx.set_option(N.CG_OPT_BOX_ORDER, order)
+    ctx.set_option(N.CG_OPT_RELAYOUT_EVERY, order)
     ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
     p = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
     for _ in range(warm):
@@ -25,7 +21,7 @@ def probe(name, pool, summation, order, flags, steps=5, warm=3, sweep=1):
     wall = (time.perf_counter() - t0) / steps
     st = sts[-1]
     tot = np.median([s.t_total_ms for s in sts])
-    print("%-10s sweep=%d sum=%d order=%d flags=%d n=%d grid=%.3f sort=%.3f force=%.3f total=%.3f ms wall=%.3f ms  "
+    print("%-10s sweep=%d sum=%d relayout=%d flags=%d n=%d grid=%.3f sort=%.3f force=%.3f total=%.3f ms wall=%.3f ms  "
           "-> %.2f G agent-upd/s (dev) evals/agent=%.2f cands/agent=%.2f" % (
           name, sweep, summation, order, flags, pool.count, st.t_grid_ms, st.t_sort_ms, st.t_force_ms, tot,
           wall * 1e3, pool.count / tot * 1e-6, st.force_evals / pool.count, st.candidates / pool.count))
@@ -42,5 +38,6 @@ if __name__ == "__main__":
         elif w == "c4f": pool = workloads.c4(PrecisionMode.FP32)
         elif w.startswith("c3_"): pool = workloads.c3(float(w[3:]))
         for summ in [int(x) for x in os.environ.get("SUMS", "0,1").split(",")]:
-            for order in [int(x) for x in os.environ.get("ORDERS", "0,1").split(",")]:
-                probe(w, pool, summ, order, 1, sweep=int(os.environ.get("SWEEP", "2")))
+            for order in [int(x) for x in os.environ.get("RELAYOUT", "1").split(",")]:
+                probe(w, pool, summ, order, int(os.environ.get("FLAGS", "1")),
+                      sweep=int(os.environ.get("SWEEP", "1")))
