@@ -28,11 +28,14 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/cellgrid_b200.h"
 #include "common.cuh"
 #include "grid.cuh"
 #include "sweep.cuh"
 #include "sweep7.cuh"
+#include "sweep_tile.cuh"
 
 using namespace cg;
 
@@ -53,6 +56,10 @@ struct Buffers {
     void *disp[3] = {nullptr, nullptr, nullptr};
     int2 *key_rank = nullptr;
     int *tmp = nullptr, *idx = nullptr, *skey = nullptr, *pres = nullptr;
+    int *pkey[2] = {nullptr, nullptr};   // box at the last sort step (travels with the records)
+    int *ovf = nullptr;              // sweep overflow list
+    void *pscratch = nullptr;        // lazy presentation sort scratch
+    size_t pscratch_bytes = 0;
     int *rec_m = nullptr, *rec_nk = nullptr;
     float *prox = nullptr;           // Proxies: xy (4 floats per slot pair) then z
     Proxies P() const { return Proxies{prox, prox + 4 * pairs}; }
@@ -79,6 +86,7 @@ struct cg_context {
     // per-step reductions
     unsigned long long *slots = nullptr;
     unsigned long long *maxd_enc = nullptr;
+    unsigned *ovf_count = nullptr;
     unsigned long long *block_counters = nullptr;   // reference-order sweep only
     double *bbox_dev = nullptr, *bbox_host = nullptr;
     bool bbox_valid = false;
@@ -95,11 +103,14 @@ struct cg_context {
     bool relaid = false;          // storage == slot order of the current grid
     int pres_state = PRES_IDENTITY;
     bool last_record = false;
+    bool last_dense = false;
     int64_t sort_steps = 0;
+    Geometry geo_sort{};          // geometry of the last sort step (presentation order)
     // options
     int summation = SUM_UID;
-    int sweep_impl = 1;           // 0 = reference-order thread per agent, 1 = sweep7
+    int sweep_impl = 1;           // 0 = reference-order thread per agent, 1 = sweep7, 2 = smem tiles (sparse)
     int relayout_every = 1;       // relayout on every k-th sort step (1 = every sort step)
+    int path = 0;                 // 0 = auto, 1 = sparse (uid-sorted lists), 2 = dense (z-sorted boxes)
     std::string err;
 };
 
@@ -130,7 +141,7 @@ static void free_agents(cg_context *c)
     void *ptrs[] = {b.pos[0][0], b.pos[0][1], b.pos[0][2], b.pos[1][0], b.pos[1][1], b.pos[1][2],
                     b.dia[0], b.dia[1], b.adh[0], b.adh[1], b.uid[0], b.uid[1],
                     b.disp[0], b.disp[1], b.disp[2], b.key_rank, b.tmp, b.idx, b.skey, b.pres,
-                    b.rec_m, b.rec_nk, b.prox, b.stage};
+                    b.rec_m, b.rec_nk, b.prox, b.stage, b.pkey[0], b.pkey[1], b.pscratch, b.ovf};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     c->b = Buffers{};
@@ -150,7 +161,7 @@ static int alloc_agents(cg_context *c, int64_t cap)
     }
     for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMalloc(&b.disp[a], fe));
     CUDA_TRY(c, cudaMalloc(&b.key_rank, sizeof(int2) * (size_t)cap));
-    int **ints[] = {&b.tmp, &b.idx, &b.skey, &b.pres, &b.rec_m, &b.rec_nk};
+    int **ints[] = {&b.tmp, &b.idx, &b.skey, &b.pres, &b.rec_m, &b.rec_nk, &b.pkey[0], &b.pkey[1], &b.ovf};
     for (int **p : ints) CUDA_TRY(c, cudaMalloc(p, ie));
     b.pairs = cap / 2 + 8;   // the sweep may read a few pairs past n
     CUDA_TRY(c, cudaMalloc(&b.prox, sizeof(float) * 6 * (size_t)b.pairs));
@@ -275,13 +286,17 @@ static int standalone_bbox(cg_context *c)
     return CG_OK;
 }
 
-// The reference's storage order for the current grid (see header comment).
+// The reference's storage order (see header comment): sort storage indices
+// by uid, then stably by the Morton rank of their box at the last sort step.
 static int materialize_presentation(cg_context *c)
 {
     if (c->pres_state != PRES_PENDING) return CG_OK;
-    const Geometry &g = c->geo;
+    const Geometry &g = c->geo_sort;
     cudaStream_t st = c->stream;
+    const int n = (int)c->n;
     if (c->table_dims[0] != g.dimx || c->table_dims[1] != g.dimy || c->table_dims[2] != g.dimz) {
+        int rc = ensure_boxes(c, g.nb);
+        if (rc) return rc;
         morton_table<<<std::min(cdiv(g.nb, kThreads), 148 * 16), kThreads, 0, st>>>(g, c->mrank, c->minv);
         LAUNCH_CHECK(c);
         c->launches += 1;
@@ -289,14 +304,40 @@ static int materialize_presentation(cg_context *c)
         c->table_dims[1] = g.dimy;
         c->table_dims[2] = g.dimz;
     }
-    int rc = launch_scan(c, true, g.nb, c->moff, nullptr);
-    if (rc) return rc;
-    const int n = (int)c->n;
-    presentation<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, c->b.skey, c->relaid ? nullptr : c->b.idx,
-                                                          c->offset, c->mrank, c->moff,
-                                                          c->b.uid[c->cur_attr], c->b.pres);
+    // scratch: u64 keys x2, u32 keys x2, int values x2, + cub temp
+    size_t t1 = 0, t2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (const int *)nullptr, (int *)nullptr, n, 0, 64, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, (const unsigned *)nullptr, (unsigned *)nullptr,
+                                    (const int *)nullptr, (int *)nullptr, n, 0, 32, st);
+    const size_t tb = (std::max(t1, t2) + 255) & ~size_t(255);
+    const size_t need = (size_t)n * (8 + 4 + 4 + 4) + tb + 1024;
+    if (need > c->b.pscratch_bytes) {
+        if (c->b.pscratch) cudaFree(c->b.pscratch);
+        c->b.pscratch = nullptr;
+        CUDA_TRY(c, cudaMalloc(&c->b.pscratch, need));
+        c->b.pscratch_bytes = need;
+    }
+    char *p = (char *)c->b.pscratch;
+    uint64_t *ukeys = (uint64_t *)p;  p += (size_t)n * 8;
+    int *vals0 = (int *)p;            p += (size_t)n * 4;
+    int *vals1 = (int *)p;            p += (size_t)n * 4;
+    unsigned *mk = (unsigned *)p;     p += (size_t)n * 4;
+    p = (char *)(((uintptr_t)p + 255) & ~uintptr_t(255));
+    void *temp = p;
+    // 1. uid order (uids are unique; the stage buffer holds the sorted keys)
+    iota<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, vals0);
+    size_t tt = tb;
+    CUDA_TRY(c, cub::DeviceRadixSort::SortPairs(temp, tt, c->b.uid[c->cur_attr], ukeys, vals0, vals1, n, 0, 64, st));
+    // 2. stable by Morton rank of the box at the sort step
+    morton_keys<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, vals1, c->b.pkey[c->cur_attr], c->mrank, mk);
+    int bits = 1;
+    while (bits < 31 && (1ll << bits) < (long long)g.nb) ++bits;
+    tt = tb;
+    CUDA_TRY(c, cub::DeviceRadixSort::SortPairs(temp, tt, mk, (unsigned *)ukeys, vals1, vals0, n, 0, bits, st));
+    invert_perm<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, vals0, c->b.pres);
     LAUNCH_CHECK(c);
-    c->launches += 1;
+    c->launches += 5;
     c->pres_state = PRES_VALID;
     return CG_OK;
 }
@@ -304,8 +345,8 @@ static int materialize_presentation(cg_context *c)
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
 // idx (or, when relayout, the records in slot order in the alternate buffers).
 template <typename T>
-static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, double origin[3],
-                      int64_t dims64[3])
+static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, bool sort,
+                      double origin[3], int64_t dims64[3])
 {
     const int n = (int)c->n;
     cudaStream_t st = c->stream;
@@ -319,8 +360,6 @@ static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, 
     if ((rc = host_geometry(c, c->bbox_host, ir, box_cap, g, dims64, origin))) return rc;
     const int slot = (int)(c->steps_done % kRing);
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][0], st));
-    // the previous grid is about to be overwritten: keep its presentation order
-    if ((rc = materialize_presentation(c))) return rc;
     if ((rc = ensure_boxes(c, g.nb))) return rc;
     c->geo = g;
     c->bd = make_decode(g);
@@ -332,24 +371,47 @@ static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, 
     LAUNCH_CHECK(c);
     c->launches += 1;
     if ((rc = launch_scan(c, false, g.nb, c->offset, stat))) return rc;
-    place<<<nblk, kThreads, 0, st>>>(n, c->b.key_rank, c->offset, c->b.tmp);
-    LAUNCH_CHECK(c);
-    c->launches += 1;
-    CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
+    // sparse pools (few agents per box): the scatter is the CSR; dense pools
+    // also order each box by (z, uid) so column runs can be cut on z
+    const double surv = 4.19 * (double)n / (double)g.nb;   // expected survivors per agent
+    const bool dense = c->path == 2 || (c->path == 0 && surv > 10.0);
     const int a = c->cur_attr, o = 1 - c->cur_pos, oa = 1 - c->cur_attr;
-    if (relayout) {
-        order_gather<T, true><<<nblk, kThreads, 0, st>>>(
-            n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, x, y, z, (T *)c->b.dia[a],
-            (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(), nullptr, (T *)c->b.pos[o][0],
-            (T *)c->b.pos[o][1], (T *)c->b.pos[o][2], (T *)c->b.dia[oa], (T *)c->b.adh[oa], c->b.uid[oa]);
+    int *pk = sort ? c->b.pkey[a] : nullptr;
+    if (!dense) {
+        place_full<T><<<nblk, kThreads, 0, st>>>(n, g, c->bd, c->b.key_rank, c->offset, x, y, z, c->b.idx,
+                                                 c->b.skey, c->b.P(), pk);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
+        if (relayout) {
+            relayout_records<T><<<nblk, kThreads, 0, st>>>(
+                n, c->b.idx, x, y, z, (T *)c->b.dia[a], (T *)c->b.adh[a], c->b.uid[a], pk,
+                (T *)c->b.pos[o][0], (T *)c->b.pos[o][1], (T *)c->b.pos[o][2], (T *)c->b.dia[oa],
+                (T *)c->b.adh[oa], c->b.uid[oa], c->b.pkey[oa]);
+            LAUNCH_CHECK(c);
+            c->launches += 1;
+        }
     } else {
-        order_gather<T, false><<<nblk, kThreads, 0, st>>>(
-            n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, x, y, z, (T *)c->b.dia[a],
-            (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr, nullptr,
-            nullptr, nullptr, nullptr);
+        place<<<nblk, kThreads, 0, st>>>(n, c->b.key_rank, c->offset, c->b.tmp);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
+        if (relayout) {
+            order_gather<T, true><<<nblk, kThreads, 0, st>>>(
+                n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, x, y, z, (T *)c->b.dia[a],
+                (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(), nullptr, (T *)c->b.pos[o][0],
+                (T *)c->b.pos[o][1], (T *)c->b.pos[o][2], (T *)c->b.dia[oa], (T *)c->b.adh[oa], c->b.uid[oa],
+                sort ? c->b.pkey[oa] : nullptr);
+        } else {
+            order_gather<T, false><<<nblk, kThreads, 0, st>>>(
+                n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, x, y, z, (T *)c->b.dia[a],
+                (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr, nullptr,
+                nullptr, nullptr, nullptr, pk);
+        }
+        LAUNCH_CHECK(c);
+        c->launches += 1;
     }
-    LAUNCH_CHECK(c);
-    c->launches += 1;
+    c->last_dense = dense;
     if (relayout) {
         c->cur_pos = o;
         c->cur_attr = oa;
@@ -357,23 +419,75 @@ static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, 
     } else {
         c->relaid = false;
     }
+    if (sort) c->geo_sort = g;
     c->have_grid = true;
     return CG_OK;
 }
 
-template <typename T, int SUM>
-static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A, int ks)
+template <typename T, bool UID, bool ZS, int KS, bool FLUSH, int MINB>
+static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
 {
-    const int nblk = cdiv(A.n, kThreads);
     cudaStream_t st = c->stream;
-    // survivor-list capacity by expected survivors per agent; dense pools
-    // evaluate the list whenever it fills (stencil order), sparse pools walk
-    // again on the rare overflow
-    if (SUM == SUM_UID || ks <= 16) sweep7_kernel<T, SUM, 16, false><<<nblk, kThreads, 0, st>>>(A);
-    else if (ks <= 32) sweep7_kernel<T, SUM_STENCIL, 32, false><<<nblk, kThreads, 0, st>>>(A);
-    else sweep7_kernel<T, SUM_STENCIL, 32, true><<<nblk, kThreads, 0, st>>>(A);
+    CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
+    sweep7_kernel<T, UID, ZS, KS, FLUSH, MINB><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
     LAUNCH_CHECK(c);
+    c->launches += 1;
+    if (!FLUSH) {   // agents with more than KS survivors (none in most steps)
+        sweep7_overflow<T, UID, ZS, KS><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+    }
     return CG_OK;
+}
+
+// Tile shape of the sparse-path sweep: 4 x 4 columns x TZ boxes with about
+// 240 core agents; staging capacity 1.25x the expected halo population.
+static TileCfg choose_tile(const Geometry &g, int64_t n)
+{
+    const double rho = (double)n / (double)g.nb;
+    TileCfg C;
+    C.tx = std::min(4, g.dimx);
+    C.ty = std::min(4, g.dimy);
+    C.tz = (int)std::lround(240.0 / (C.tx * C.ty * std::max(rho, 1e-3)));
+    C.tz = std::max(1, std::min(C.tz, std::min(64, g.dimz)));
+    C.ntx = cdiv(g.dimx, C.tx);
+    C.nty = cdiv(g.dimy, C.ty);
+    C.ntz = cdiv(g.dimz, C.tz);
+    C.max_cols = (C.tx + 2) * (C.ty + 2);
+    const double halo = (double)C.max_cols * (C.tz + 2) * rho;
+    C.cap = ((int)(1.25 * halo + 96.0) + 1) & ~1;
+    const double E = g.L * (double)std::max(C.tx + 2, std::max(C.ty + 2, C.tz + 2));
+    C.margin = (float)(64.0 * E * 5.9604644775390625e-8);
+    return C;
+}
+
+template <typename T>
+static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
+{
+    if (!c->last_dense) {
+        // sparse: shared-memory tiles, survivors summed in uid order (deterministic
+        // and bit-identical to the reference whatever the slot order in a box);
+        // agents with many survivors / tiles over capacity go to the overflow kernel
+        cudaStream_t st = c->stream;
+        const TileCfg C = choose_tile(c->geo, c->n);
+        const size_t sm = TileLayout<T>(C.cap, C.max_cols, C.tz).total;
+        const long long ntiles = (long long)C.ntx * C.nty * C.ntz;
+        if (c->sweep_impl == 2 && sm <= 160 * 1024 && ntiles < INT32_MAX) {
+            auto k = sweep_tile_kernel<T, 16>;
+            CUDA_TRY(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
+            k<<<(int)ntiles, kThreads, sm, st>>>(A, C);
+            LAUNCH_CHECK(c);
+            sweep7_overflow<T, true, false, 16><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
+            LAUNCH_CHECK(c);
+            c->launches += 2;
+            return CG_OK;
+        }
+        return launch_sweep7_k<T, true, false, 16, false, 4>(c, A);
+    }
+    if (c->summation == SUM_UID) return launch_sweep7_k<T, true, true, 16, false, 3>(c, A);
+    // dense, stencil order: the list is evaluated whenever it fills
+    return launch_sweep7_k<T, false, true, 32, true, 3>(c, A);
 }
 
 template <typename T>
@@ -469,19 +583,16 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
             A.shell_hi[q] = hi - B;
         }
     }
-    // survivors per agent ~ 4.19 * (agents per box) (contact ball / box volume)
-    const double rho = (double)n / (double)c->geo.nb;
-    const double surv = 4.19 * rho;   // contact ball / box volume
-    const int ks = surv <= 9.0 ? 16 : (surv <= 20.0 ? 32 : 64);
-    int rc = c->summation == SUM_UID ? launch_sweep7<T, SUM_UID>(c, A, ks)
-                                     : launch_sweep7<T, SUM_STENCIL>(c, A, ks);
+    A.ovf = c->b.ovf;
+    A.ovf_count = c->ovf_count;
+    int rc = launch_sweep7<T>(c, A);
     if (rc) return rc;
     unsigned long long *stat = c->stat_dev + (c->steps_done % kRing) * kStatSlots;
     // frozen: positions (and so the bbox in bbox_host) are unchanged
     finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, stat, c->bbox_dev,
                                          FINISH_COUNTERS | (freeze ? 0 : FINISH_BBOX));
     LAUNCH_CHECK(c);
-    c->launches += 2;
+    c->launches += 1;
     if (!freeze)
         CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
     c->bbox_valid = true;
@@ -517,7 +628,7 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
     int rc;
     // build_grid records event 0 after the bbox readback + host geometry, so
     // the per-phase times are device times
-    if ((rc = build_grid<T>(c, ir, box_cap, relayout, origin, dims64))) return rc;
+    if ((rc = build_grid<T>(c, ir, box_cap, relayout, sort, origin, dims64))) return rc;
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
     if (sort) {
         c->sort_steps++;
@@ -622,6 +733,7 @@ int cg_create(int device, int precision, cg_context **out)
     chk(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     chk(cudaMalloc(&c->slots, sizeof(unsigned long long) * kSlots * kSlotWords));
     chk(cudaMalloc(&c->maxd_enc, sizeof(unsigned long long)));
+    chk(cudaMalloc(&c->ovf_count, sizeof(unsigned)));
     chk(cudaMalloc(&c->block_counters, sizeof(unsigned long long) * 3 * kMaxCounterBlocks));
     chk(cudaMalloc(&c->bbox_dev, sizeof(double) * 8));
     chk(cudaMallocHost(&c->bbox_host, sizeof(double) * 8));
@@ -651,7 +763,7 @@ void cg_destroy(cg_context *c)
     int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->moff};
     for (int *p : ptrs)
         if (p) cudaFree(p);
-    void *vptrs[] = {c->scan_status, c->slots, c->maxd_enc, c->block_counters, c->bbox_dev, c->stat_dev};
+    void *vptrs[] = {c->scan_status, c->slots, c->maxd_enc, c->ovf_count, c->block_counters, c->bbox_dev, c->stat_dev};
     for (void *p : vptrs)
         if (p) cudaFree(p);
     if (c->bbox_host) cudaFreeHost(c->bbox_host);
@@ -690,12 +802,16 @@ int cg_set_option(cg_context *c, int key, int value)
         c->summation = value;
         return CG_OK;
     }
-    if (key == CG_OPT_SWEEP && (value == 0 || value == 1)) {
+    if (key == CG_OPT_SWEEP && value >= 0 && value <= 2) {
         c->sweep_impl = value;
         return CG_OK;
     }
     if (key == CG_OPT_RELAYOUT_EVERY && value >= 1) {
         c->relayout_every = value;
+        return CG_OK;
+    }
+    if (key == CG_OPT_PATH && value >= 0 && value <= 2) {
+        c->path = value;
         return CG_OK;
     }
     return fail(c, CG_ERR_VALUE, "bad option %d=%d", key, value);
@@ -792,8 +908,8 @@ int cg_build_grid(cg_context *c, double interaction_radius, int64_t box_cap, cg_
     int64_t dims64[3];
     const int slot = (int)(c->steps_done % kRing);
     const int rc = c->prec == CG_FP64
-                       ? build_grid<double>(c, interaction_radius, box_cap, false, origin, dims64)
-                       : build_grid<float>(c, interaction_radius, box_cap, false, origin, dims64);
+                       ? build_grid<double>(c, interaction_radius, box_cap, false, false, origin, dims64)
+                       : build_grid<float>(c, interaction_radius, box_cap, false, false, origin, dims64);
     if (rc) return rc;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (stats) {
@@ -942,13 +1058,13 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
             nn, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, (double *)c->b.pos[0][0],
             (double *)c->b.pos[0][1], (double *)c->b.pos[0][2], (double *)c->b.dia[0],
             (double *)c->b.adh[0], c->b.uid[0], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr,
-            nullptr, nullptr, nullptr, nullptr);
+            nullptr, nullptr, nullptr, nullptr, nullptr);
     else
         order_gather<float, false><<<nblk, kThreads, 0, st>>>(
             nn, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, (float *)c->b.pos[0][0],
             (float *)c->b.pos[0][1], (float *)c->b.pos[0][2], (float *)c->b.dia[0],
             (float *)c->b.adh[0], c->b.uid[0], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr,
-            nullptr, nullptr, nullptr, nullptr);
+            nullptr, nullptr, nullptr, nullptr, nullptr);
     LAUNCH_CHECK(c);
     c->launches += 5;
     c->relaid = false;

@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kThreads) order_gather(
     const T *__restrict__ z, const T *__restrict__ d, const T *__restrict__ adh,
     const uint64_t *__restrict__ uid, int *__restrict__ skey, Proxies prox,
     int *__restrict__ idx, T *__restrict__ ox_, T *__restrict__ oy_, T *__restrict__ oz_,
-    T *__restrict__ od, T *__restrict__ oadh, uint64_t *__restrict__ ouid)
+    T *__restrict__ od, T *__restrict__ oadh, uint64_t *__restrict__ ouid, int *__restrict__ pkey)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
@@ -470,35 +470,77 @@ __global__ void __launch_bounds__(kThreads) order_gather(
         od[dst] = di;
         oadh[dst] = adh[i];
         ouid[dst] = ui;
+        if (pkey) pkey[dst] = k;
     } else {
         idx[dst] = i;
+        if (pkey) pkey[i] = k;
     }
+}
+
+// Sparse pools: the counting-sort scatter is the whole CSR build -- members
+// of a box keep their (arbitrary) atomic rank, the sweep sums each agent's
+// pairs in uid order.  One thread per storage index writes idx / skey / the
+// proxies of its slot, and (sort steps) its box key for the lazy reference
+// storage order.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) place_full(int n, Geometry g, BoxDecode bd,
+                                                       const int2 *__restrict__ key_rank,
+                                                       const int *__restrict__ offset, const T *__restrict__ x,
+                                                       const T *__restrict__ y, const T *__restrict__ z,
+                                                       int *__restrict__ idx, int *__restrict__ skey,
+                                                       Proxies prox, int *__restrict__ pkey)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int2 kr = key_rank[i];
+    const int slot = __ldg(offset + kr.x) + kr.y;
+    int ix, iy, iz;
+    decode_box(bd, kr.x, ix, iy, iz);
+    idx[slot] = i;
+    skey[slot] = kr.x;
+    put_proxy<T>(prox, g, slot, ix, iy, x[i], y[i], z[i]);
+    if (pkey) pkey[i] = kr.x;
+}
+
+// Move the records into slot order (locality for the sweep; the paper's
+// Z-order data sort).  pkey travels with them.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) relayout_records(
+    int n, const int *__restrict__ idx, const T *__restrict__ x, const T *__restrict__ y,
+    const T *__restrict__ z, const T *__restrict__ d, const T *__restrict__ adh,
+    const uint64_t *__restrict__ uid, const int *__restrict__ pkey, T *__restrict__ ox_,
+    T *__restrict__ oy_, T *__restrict__ oz_, T *__restrict__ od, T *__restrict__ oadh,
+    uint64_t *__restrict__ ouid, int *__restrict__ opkey)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int i = idx[s];
+    ox_[s] = x[i];
+    oy_[s] = y[i];
+    oz_[s] = z[i];
+    od[s] = d[i];
+    oadh[s] = adh[i];
+    ouid[s] = uid[i];
+    if (pkey) opkey[s] = pkey[i];
 }
 
 // ---------------------------------------------------------------- presentation
 // The reference's storage order after a sorted step (morton.py:67-74,
-// lexsort((uid, code))): pres[storage index] = position in that order =
-// moff[mrank[box]] + (rank of the uid among the box's members).
-__global__ void __launch_bounds__(kThreads) presentation(int n, const int *__restrict__ skey,
-                                                         const int *__restrict__ idx,
-                                                         const int *__restrict__ offset,
-                                                         const int *__restrict__ mrank,
-                                                         const int *__restrict__ moff,
-                                                         const uint64_t *__restrict__ uid,
-                                                         int *__restrict__ pres)
+// lexsort((uid, code))) is materialised lazily, at download/export time, from
+// pkey (box of every agent at the last sort step) and uid:
+//   1. sort storage indices by uid,  2. stable-sort them by Morton rank of pkey,
+//   3. pres[order[r]] = r.
+__global__ void morton_keys(int n, const int *__restrict__ order, const int *__restrict__ pkey,
+                            const int *__restrict__ mrank, unsigned *__restrict__ out)
 {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    const int k = skey[s];
-    const int i = idx ? idx[s] : s;
-    const int o0 = __ldg(offset + k), o1 = __ldg(offset + k + 1);
-    const uint64_t ui = uid[i];
-    int q = 0;
-    for (int t = o0; t < o1; ++t) {
-        const int j = idx ? __ldg(idx + t) : t;
-        q += uid[j] < ui;
-    }
-    pres[i] = __ldg(moff + __ldg(mrank + k)) + q;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) out[r] = (unsigned)__ldg(mrank + pkey[order[r]]);
+}
+
+__global__ void invert_perm(int n, const int *__restrict__ order, int *__restrict__ pres)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) pres[order[r]] = r;
 }
 
 // dst[pres[i]] = src[i] (download / export in the reference's order)

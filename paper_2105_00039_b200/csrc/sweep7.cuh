@@ -33,10 +33,6 @@
 #include "grid.cuh"
 #include "sweep.cuh"
 
-#ifndef CG_SWEEP_MINB
-#define CG_SWEEP_MINB 4   // resident CTAs per SM the register allocation must allow (measured best)
-#endif
-
 namespace cg {
 
 template <typename T>
@@ -58,6 +54,8 @@ struct Sweep7Args {
     int *rec_m, *rec_nk;        // storage order, nullptr unless recording
     unsigned long long *slots;  // per-step reduction slots
     double shell_lo[3], shell_hi[3];   // bbox shell: old lo + max move, old hi - max move
+    int *ovf;                   // slots of agents deferred to the overflow kernel
+    unsigned *ovf_count;
 };
 
 // packed fp32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2)
@@ -91,18 +89,21 @@ __device__ __forceinline__ void f2_unpack(f32x2 v, float &lo, float &hi)
     asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
 
-template <typename T, int SUM, int KS, bool FLUSH>
-__global__ void __launch_bounds__(kThreads, CG_SWEEP_MINB) sweep7_kernel(Sweep7Args<T> A)
+// UIDMODE: sum each agent's pairs in ascending uid (lists sorted per lane);
+// ZSORTED: members of a box are z-sorted (dense path), so a column run can be
+// cut at z + reach; FLUSH: evaluate the list whenever it fills (stencil order).
+// DEFER: an agent with more than KS survivors is handed to the overflow
+// kernel (slot appended to A.ovf) instead of taking further walks here.
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, bool DEFER>
+__device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s, unsigned &c_m,
+                                            unsigned &c_nk, unsigned &c_nd)
 {
-    constexpr bool UIDMODE = SUM == SUM_UID;
     __shared__ int lst[KS][kThreads];
     __shared__ uint64_t ukey[UIDMODE ? KS : 1][kThreads];
+    static_assert(!(UIDMODE && FLUSH), "uid order needs the whole list");
 #define LST(k) lst[k][threadIdx.x]
 #define UKEY(k) ukey[k][threadIdx.x]
-
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned c_m = 0, c_nk = 0, c_nd = 0;
-    if (s < A.n) {
+    {
         const int key = __ldg(A.skey + s);
         int ix, iy, iz;
         decode_box(A.bd, key, ix, iy, iz);
@@ -160,9 +161,11 @@ __global__ void __launch_bounds__(kThreads, CG_SWEEP_MINB) sweep7_kernel(Sweep7A
                             if (pb) visit(ta + 1);
                             after();
                         }
-                        float za, zb;
-                        f2_unpack(zz, za, zb);
-                        if (zb > zhi) break;   // z-sorted run (zb past t1 only ends the loop sooner)
+                        if (ZSORTED) {
+                            float za, zb;
+                            f2_unpack(zz, za, zb);
+                            if (zb > zhi) break;   // z-sorted run (zb past t1 only ends the loop sooner)
+                        }
                     }
                 }
             }
@@ -247,6 +250,10 @@ __global__ void __launch_bounds__(kThreads, CG_SWEEP_MINB) sweep7_kernel(Sweep7A
                     ++total;
                 },
                 [] {});
+            if (DEFER && total > KS) {
+                A.ovf[atomicAdd(A.ovf_count, 1u)] = s;
+                return;
+            }
             evaluate(ns);
             for (int done = KS; done < total; done += KS) {
                 int seen = 0;
@@ -265,16 +272,17 @@ __global__ void __launch_bounds__(kThreads, CG_SWEEP_MINB) sweep7_kernel(Sweep7A
             int ns = 0, total = 0;
             m = walk(
                 [&](int t) {
-                    if (ns < KS) {
-                        LST(ns) = t;
-                        UKEY(ns) = cand_uid(t);
-                        ++ns;
-                    }
+                    if (ns < KS) LST(ns++) = t;
                     ++total;
                 },
                 [] {});
+            if (DEFER && total > KS) {
+                A.ovf[atomicAdd(A.ovf_count, 1u)] = s;
+                return;
+            }
             if (total <= KS) {
                 // insertion sort by uid, then one evaluation in uid order
+                for (int p = 0; p < ns; ++p) UKEY(p) = cand_uid(LST(p));
                 for (int p = 1; p < ns; ++p) {
                     const uint64_t u = UKEY(p);
                     const int v = LST(p);
@@ -352,23 +360,48 @@ __global__ void __launch_bounds__(kThreads, CG_SWEEP_MINB) sweep7_kernel(Sweep7A
             A.rec_m[a] = m;
             A.rec_nk[a] = nk;
         }
-        c_m = (unsigned)m;
-        c_nk = (unsigned)nk;
-        c_nd = (unsigned)nd;
+        c_m += (unsigned)m;
+        c_nk += (unsigned)nk;
+        c_nd += (unsigned)nd;
     }
 #undef LST
 #undef UKEY
-    // counters: one REDUX per warp, one atomic per warp and counter
+}
+
+// counters: one REDUX per warp, one atomic per warp and counter
+__device__ __forceinline__ void warp_counters(unsigned long long *slots, unsigned c_m, unsigned c_nk,
+                                              unsigned c_nd)
+{
     c_m = __reduce_add_sync(0xffffffffu, c_m);
     c_nk = __reduce_add_sync(0xffffffffu, c_nk);
     c_nd = __reduce_add_sync(0xffffffffu, c_nd);
     if ((threadIdx.x & 31) == 0) {
-        unsigned long long *slot = A.slots + (blockIdx.x % kSlots) * kSlotWords;
-        atomicAdd(slot + 6, (unsigned long long)c_nk);
-        atomicAdd(slot + 7, (unsigned long long)c_m);
+        unsigned long long *slot = slots + (blockIdx.x % kSlots) * kSlotWords;
+        if (c_nk) atomicAdd(slot + 6, (unsigned long long)c_nk);
+        if (c_m) atomicAdd(slot + 7, (unsigned long long)c_m);
         if (c_nd) atomicAdd(slot + 8, (unsigned long long)c_nd);
     }
 }
 
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) sweep7_kernel(Sweep7Args<T> A)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned c_m = 0, c_nk = 0, c_nd = 0;
+    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true>(A, s, c_m, c_nk, c_nd);
+    warp_counters(A.slots, c_m, c_nk, c_nd);
+}
+
+// agents deferred by sweep7_kernel (more than KS survivors): grid-stride over
+// the device-side list, further walks per agent
+template <typename T, bool UIDMODE, bool ZSORTED, int KS>
+__global__ void __launch_bounds__(kThreads) sweep7_overflow(Sweep7Args<T> A)
+{
+    unsigned c_m = 0, c_nk = 0, c_nd = 0;
+    const unsigned cnt = *A.ovf_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
+        sweep_agent<T, UIDMODE, ZSORTED, KS, false, false>(A, A.ovf[k], c_m, c_nk, c_nd);
+    warp_counters(A.slots, c_m, c_nk, c_nd);
+}
 
 }  // namespace cg

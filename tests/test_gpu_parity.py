@@ -27,12 +27,13 @@ def _native():
     return _native
 
 
-def _ctx(dtype, summation="uid", sweep="v7", relayout_every=1):
+def _ctx(dtype, summation="uid", sweep="v7", relayout_every=1, path="auto"):
     N = _native()
     ctx = N.Context(0, dtype)
     ctx.set_option(N.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[summation])
-    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "v7": 1}[sweep])
+    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "v7": 1, "tile": 2}[sweep])
     ctx.set_option(N.CG_OPT_RELAYOUT_EVERY, relayout_every)
+    ctx.set_option(N.CG_OPT_PATH, {"auto": 0, "sparse": 1, "dense": 2}[path])
     return ctx
 
 
@@ -68,10 +69,12 @@ def _reference_state(g, k):
             g["in_adh"][order], uid]
 
 
-@pytest.mark.parametrize("sweep,relayout", [("v7", 1), ("v7", 2), ("v7", 1000), ("agent", 1)])
+@pytest.mark.parametrize("sweep,relayout,path", [
+    ("v7", 1, "auto"), ("v7", 1, "sparse"), ("v7", 1, "dense"), ("v7", 2, "sparse"),
+    ("v7", 3, "dense"), ("v7", 1000, "sparse"), ("tile", 1, "sparse"), ("agent", 1, "auto")])
 @pytest.mark.parametrize("summation", ["uid", "stencil"])
 @pytest.mark.parametrize("name", golden_names())
-def test_golden(cuda_required, name, summation, sweep, relayout):
+def test_golden(cuda_required, name, summation, sweep, relayout, path):
     """uid mode chains all steps on the device (bit-exact end to end); stencil
     mode restarts every step from the reference's state, because its last-ulp
     differences legitimately move later bounding boxes.  relayout = the device
@@ -80,11 +83,13 @@ def test_golden(cuda_required, name, summation, sweep, relayout):
     g = load_golden(name)
     dt = g["in_px"].dtype
     N = _native()
-    ctx = _ctx(dt, summation, sweep=sweep, relayout_every=relayout)
+    ctx = _ctx(dt, summation, sweep=sweep, relayout_every=relayout, path=path)
+    # the sparse path always sums in uid order (bit-exact)
+    exact = summation == "uid" or (sweep in ("v7", "tile") and path == "sparse")
     every = int(g["sort_every"])
     for k in range(int(g["steps"])):
         s = "s%d_" % k
-        if k == 0 or summation == "stencil":
+        if k == 0 or not exact:
             ctx.upload(*_reference_state(g, k))
         degenerate = int(g[s + "ndeg"]) > 0
         flags = N.CG_STEP_RECORD
@@ -112,7 +117,7 @@ def test_golden(cuda_required, name, summation, sweep, relayout):
         assert np.array_equal(nk, g[s + "nk"])
         pairs = (("dx", "dx"), ("dy", "dy"), ("dz", "dz"),
                  ("px", "out_px"), ("py", "out_py"), ("pz", "out_pz"))
-        if summation == "uid" and not degenerate:
+        if exact and not degenerate:
             for mine, ref in pairs:
                 assert np.array_equal(cols[mine], g[s + ref]), (k, mine)
         else:
