@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CG_ABI_VERSION 2
+#define CG_ABI_VERSION 3
 
 /* status codes */
 #define CG_OK 0
@@ -130,6 +130,39 @@ int cg_force_phase(cg_context *ctx, int64_t n, const void *px, const void *py, c
                    const int64_t *box_index, int64_t dimx, int64_t dimy, int64_t dimz,
                    const void *params7, void *out_dx, void *out_dy, void *out_dz,
                    int64_t counters[3]);
+
+/* ---- x-slab decomposition (multi-GPU).  The reference has no
+ * distributed layer: these entry points carry the same step across ranks,
+ * one context per GPU.  Device buffers (send/recv) are raw device pointers
+ * owned by the caller (e.g. torch CUDA tensors handed to NCCL); records are
+ * cg_record_bytes() each.  Per step, on every rank:
+ *   cg_local_bbox -> all-reduce (min/min/min/max/max/max/max) -> cg_slab_plan
+ *   -> all-to-all counts -> cg_slab_migrate(send) -> all-to-all records ->
+ *   cg_slab_accept(recv) -> cg_slab_halo(NULL) / cg_slab_halo(send) ->
+ *   exchange with rank-1 / rank+1 -> cg_slab_set_ghosts(recv) -> cg_slab_step.
+ * Owned agents' results are those of a single-GPU step over the global pool. */
+int64_t cg_record_bytes(const cg_context *ctx);
+/* Pre-size the agent buffers (before cg_upload) for arrivals and ghosts. */
+int cg_reserve(cg_context *ctx, int64_t capacity);
+/* Exact bbox of the owned agents (min xyz, max xyz) + max diameter. */
+int cg_local_bbox(cg_context *ctx, double out[7]);
+/* Geometry from the global bbox (spatial.py:99-116; GridOverflowError as
+ * cg_step), slab planes X_k = floor(k dimx / world): planes = {X_rank,
+ * X_rank+1}; counts[k] = owned agents whose box plane rank k owns. */
+int cg_slab_plan(cg_context *ctx, const double bbox[7], double interaction_radius, int64_t box_cap,
+                 int world, int rank, int64_t *counts, int64_t planes[2]);
+/* Departing agents -> send (grouped by destination rank, ascending, own rank
+ * skipped); the remaining agents are compacted. */
+int cg_slab_migrate(cg_context *ctx, void *send);
+/* Append count received records as owned agents. */
+int cg_slab_accept(cg_context *ctx, const void *recv, int64_t count);
+/* send == NULL: counts[0] / counts[1] = owned agents in plane X_rank (for
+ * rank-1) / plane X_rank+1 - 1 (for rank+1); else pack them in that order. */
+int cg_slab_halo(cg_context *ctx, void *send, int64_t counts[2]);
+/* This step's ghosts (candidates only, dropped after cg_slab_step). */
+int cg_slab_set_ghosts(cg_context *ctx, const void *recv, int64_t count);
+/* The mechanical step on the owned agents over the slab's sub-grid. */
+int cg_slab_step(cg_context *ctx, const double params[5], int flags, cg_step_stats *stats);
 
 #ifdef __cplusplus
 }

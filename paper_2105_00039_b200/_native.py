@@ -28,7 +28,9 @@ EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_
             "cg_set_option", "cg_stream", "cg_upload", "cg_download", "cg_count", "cg_step",
             "cg_fetch_stats", "cg_build_grid", "cg_synchronize", "cg_grid_export",
             "cg_record_export", "cg_box_ids", "cg_force_phase", "cg_launch_count",
-            "cg_host_alloc", "cg_host_free")
+            "cg_host_alloc", "cg_host_free", "cg_record_bytes", "cg_reserve", "cg_local_bbox",
+            "cg_slab_plan", "cg_slab_migrate", "cg_slab_accept", "cg_slab_halo",
+            "cg_slab_set_ghosts", "cg_slab_step")
 
 
 class GridOverflowError(RuntimeError):
@@ -94,12 +96,22 @@ def load():
         "cg_box_ids": ([_P, _I64, _P, _P, _P] + [ctypes.c_double] * 4 + [_I64] * 3 + [_P],
                        ctypes.c_int),
         "cg_force_phase": ([_P, _I64] + [_P] * 7 + [_I64] * 3 + [_P] * 5, ctypes.c_int),
+        "cg_record_bytes": ([_P], _I64),
+        "cg_reserve": ([_P, _I64], ctypes.c_int),
+        "cg_local_bbox": ([_P, _P], ctypes.c_int),
+        "cg_slab_plan": ([_P, _P, ctypes.c_double, _I64, ctypes.c_int, ctypes.c_int, _P, _P],
+                         ctypes.c_int),
+        "cg_slab_migrate": ([_P, _P], ctypes.c_int),
+        "cg_slab_accept": ([_P, _P, _I64], ctypes.c_int),
+        "cg_slab_halo": ([_P, _P, _P], ctypes.c_int),
+        "cg_slab_set_ghosts": ([_P, _P, _I64], ctypes.c_int),
+        "cg_slab_step": ([_P, _P, ctypes.c_int, ctypes.POINTER(StepStatsC)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
-    if L.cg_abi_version() != 2:
+    if L.cg_abi_version() != 3:
         raise NativeUnavailable("ABI version mismatch")
     _lib = L
     return L
@@ -214,6 +226,57 @@ class Context:
         bc = np.empty(num_boxes, np.int64)
         check(load().cg_grid_export(self.h, ptr(bi), ptr(bc)), self.h)
         return bi, bc
+
+    # ---- x-slab decomposition (see include/cellgrid_b200.h and distributed.py)
+    @property
+    def record_bytes(self):
+        return int(load().cg_record_bytes(self.h))
+
+    def reserve(self, capacity):
+        check(load().cg_reserve(self.h, int(capacity)), self.h)
+
+    def local_bbox(self):
+        out = np.empty(7, np.float64)
+        check(load().cg_local_bbox(self.h, ptr(out)), self.h)
+        return out
+
+    def slab_plan(self, bbox, world, rank, interaction_radius=None, box_cap=1 << 24):
+        bb = np.ascontiguousarray(bbox, np.float64)
+        counts = np.zeros(world, np.int64)
+        planes = np.zeros(2, np.int64)
+        ir = float("nan") if interaction_radius is None else float(interaction_radius)
+        check(load().cg_slab_plan(self.h, ptr(bb), ir, int(box_cap), int(world), int(rank),
+                                  ptr(counts), ptr(planes)), self.h)
+        return counts, planes
+
+    def slab_migrate(self, send_ptr):
+        check(load().cg_slab_migrate(self.h, send_ptr), self.h)
+        self.n = int(load().cg_count(self.h))
+
+    def slab_accept(self, recv_ptr, count):
+        check(load().cg_slab_accept(self.h, recv_ptr, int(count)), self.h)
+        self.n = int(load().cg_count(self.h))
+
+    def slab_halo_counts(self):
+        counts = np.zeros(2, np.int64)
+        check(load().cg_slab_halo(self.h, None, ptr(counts)), self.h)
+        return counts
+
+    def slab_halo_pack(self, send_ptr):
+        counts = np.zeros(2, np.int64)
+        check(load().cg_slab_halo(self.h, send_ptr, ptr(counts)), self.h)
+
+    def slab_set_ghosts(self, recv_ptr, count):
+        check(load().cg_slab_set_ghosts(self.h, recv_ptr, int(count)), self.h)
+
+    def slab_step(self, params5, flags=0, wait=True):
+        p = np.ascontiguousarray(params5, np.float64)
+        st = StepStatsC() if wait else None
+        check(load().cg_slab_step(self.h, ptr(p), int(flags), ctypes.byref(st) if wait else None),
+              self.h)
+        self.steps += 1
+        self.n = int(load().cg_count(self.h))
+        return st if wait else self.steps - 1
 
     def record_export(self):
         m = np.empty(self.n, np.int32)

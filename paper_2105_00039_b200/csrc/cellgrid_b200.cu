@@ -36,6 +36,7 @@
 #include "sweep.cuh"
 #include "sweep7.cuh"
 #include "sweep_tile.cuh"
+#include "slab.cuh"
 
 using namespace cg;
 
@@ -75,6 +76,7 @@ struct cg_context {
     size_t esz = 8;
     cudaStream_t stream = nullptr;
     int64_t n = 0, cap = 0;
+    int64_t n_owned = 0;          // agents this context owns; [n_owned, n) are this step's ghosts
     Buffers b;
     int cur_pos = 0, cur_attr = 0;
     // boxes
@@ -111,6 +113,22 @@ struct cg_context {
     int sweep_impl = 1;           // 0 = reference-order thread per agent, 1 = sweep7, 2 = smem tiles (sparse)
     int relayout_every = 1;       // relayout on every k-th sort step (1 = every sort step)
     int path = 0;                 // 0 = auto, 1 = sparse (uid-sorted lists), 2 = dense (z-sorted boxes)
+    // x-slab decomposition (multi-GPU)
+    struct Slab {
+        bool planned = false;
+        Geometry g{};            // global geometry of this step
+        SlabBounds B{};
+        int rank = 0, world = 1, x0 = 0, x1 = 0;
+        unsigned char *dest = nullptr;
+        int *dep = nullptr, *holes = nullptr, *movers = nullptr, *lo = nullptr, *hi = nullptr;
+        unsigned *cnt = nullptr;                 // 8 counters
+        unsigned long long *counts = nullptr;    // per destination rank
+        unsigned long long *dest_off = nullptr;
+        unsigned *cursor = nullptr;
+        int64_t cap = 0;
+        int64_t h_counts[kMaxWorld] = {};
+        unsigned h_halo[2] = {0, 0};
+    } slab;
     std::string err;
 };
 
@@ -225,6 +243,8 @@ static int host_geometry(cg_context *c, const double bb[7], double ir, int64_t b
     g.dimy = (int)dims64[1];
     g.dimz = (int)dims64[2];
     g.nb = (int)nb;
+    g.xoff = 0;
+    g.gdimx = g.dimx;
     return CG_OK;
 }
 
@@ -273,7 +293,7 @@ static int launch_scan(cg_context *c, bool morton, int nb, int *out, unsigned lo
 template <typename T>
 static int standalone_bbox(cg_context *c)
 {
-    const int n = (int)c->n;
+    const int n = (int)c->n_owned;
     cudaStream_t st = c->stream;
     T *x = (T *)c->b.pos[c->cur_pos][0], *y = (T *)c->b.pos[c->cur_pos][1], *z = (T *)c->b.pos[c->cur_pos][2];
     bbox_slots<T><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(n, x, y, z, c->slots);
@@ -345,10 +365,12 @@ static int materialize_presentation(cg_context *c)
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
 // idx (or, when relayout, the records in slot order in the alternate buffers).
 template <typename T>
+static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort);
+
+template <typename T>
 static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, bool sort,
                       double origin[3], int64_t dims64[3])
 {
-    const int n = (int)c->n;
     cudaStream_t st = c->stream;
     int rc;
     if (!c->bbox_valid) {
@@ -358,6 +380,16 @@ static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, 
     }
     Geometry g;
     if ((rc = host_geometry(c, c->bbox_host, ir, box_cap, g, dims64, origin))) return rc;
+    return build_grid_geo<T>(c, g, relayout, sort);
+}
+
+// Grid rebuild for a given geometry (global, or a slab's sub-grid).
+template <typename T>
+static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort)
+{
+    const int n = (int)c->n;
+    cudaStream_t st = c->stream;
+    int rc;
     const int slot = (int)(c->steps_done % kRing);
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][0], st));
     if ((rc = ensure_boxes(c, g.nb))) return rc;
@@ -585,6 +617,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     }
     A.ovf = c->b.ovf;
     A.ovf_count = c->ovf_count;
+    A.n_owned = (int)c->n_owned;
     int rc = launch_sweep7<T>(c, A);
     if (rc) return rc;
     unsigned long long *stat = c->stat_dev + (c->steps_done % kRing) * kStatSlots;
@@ -693,6 +726,229 @@ static int download_column(cg_context *c, const void *src, void *dst, size_t w)
     LAUNCH_CHECK(c);
     c->launches += 1;
     CUDA_TRY(c, cudaMemcpyAsync(dst, c->b.stage, w * n, cudaMemcpyDeviceToHost, st));
+    return CG_OK;
+}
+
+// ---------------------------------------------------------------- x-slabs
+static int slab_alloc(cg_context *c)
+{
+    auto &S = c->slab;
+    if (S.cap >= c->cap && S.cnt) return CG_OK;
+    void *ptrs[] = {S.dest, S.dep, S.holes, S.movers, S.lo, S.hi, S.cnt, S.counts, S.dest_off, S.cursor};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    const size_t n = (size_t)std::max<int64_t>(c->cap, 1);
+    CUDA_TRY(c, cudaMalloc(&S.dest, n));
+    int **ints[] = {&S.dep, &S.holes, &S.movers, &S.lo, &S.hi};
+    for (int **p : ints) CUDA_TRY(c, cudaMalloc(p, sizeof(int) * n));
+    CUDA_TRY(c, cudaMalloc(&S.cnt, sizeof(unsigned) * 8));
+    CUDA_TRY(c, cudaMalloc(&S.counts, sizeof(unsigned long long) * kMaxWorld));
+    CUDA_TRY(c, cudaMalloc(&S.dest_off, sizeof(unsigned long long) * kMaxWorld));
+    CUDA_TRY(c, cudaMalloc(&S.cursor, sizeof(unsigned) * kMaxWorld));
+    S.cap = c->cap;
+    return CG_OK;
+}
+
+template <typename T>
+static SlabCols<T> cur_cols(cg_context *c)
+{
+    SlabCols<T> C;
+    C.x = (T *)c->b.pos[c->cur_pos][0];
+    C.y = (T *)c->b.pos[c->cur_pos][1];
+    C.z = (T *)c->b.pos[c->cur_pos][2];
+    C.d = (T *)c->b.dia[c->cur_attr];
+    C.adh = (T *)c->b.adh[c->cur_attr];
+    C.uid = c->b.uid[c->cur_attr];
+    C.dx = (T *)c->b.disp[0];
+    C.dy = (T *)c->b.disp[1];
+    C.dz = (T *)c->b.disp[2];
+    return C;
+}
+
+template <typename T>
+static int slab_plan_t(cg_context *c, const double bb[7], double ir, int64_t box_cap, int world, int rank,
+                       int64_t *counts, int64_t planes[2])
+{
+    auto &S = c->slab;
+    int rc;
+    if ((rc = slab_alloc(c))) return rc;
+    Geometry g;
+    int64_t dims64[3];
+    double origin[3];
+    if ((rc = host_geometry(c, bb, ir, box_cap, g, dims64, origin))) return rc;
+    if (g.dimx < world)
+        return fail(c, CG_ERR_VALUE, "grid of %d x-planes is too narrow for %d slabs", g.dimx, world);
+    S.g = g;
+    S.world = world;
+    S.rank = rank;
+    S.B.world = world;
+    for (int k = 0; k <= world; ++k) S.B.x[k] = (int)(((int64_t)k * g.dimx) / world);
+    S.x0 = S.B.x[rank];
+    S.x1 = S.B.x[rank + 1];
+    planes[0] = S.x0;
+    planes[1] = S.x1;
+    cudaStream_t st = c->stream;
+    CUDA_TRY(c, cudaMemsetAsync(S.counts, 0, sizeof(unsigned long long) * kMaxWorld, st));
+    const int n = (int)c->n_owned;
+    if (n > 0) {
+        slab_dest<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, g, S.B, (const T *)c->b.pos[c->cur_pos][0], S.dest,
+                                                              S.counts);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+    }
+    unsigned long long h[kMaxWorld];
+    CUDA_TRY(c, cudaMemcpyAsync(h, S.counts, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    for (int k = 0; k < world; ++k) counts[k] = S.h_counts[k] = (int64_t)h[k];
+    S.planned = true;
+    return CG_OK;
+}
+
+template <typename T>
+static int slab_migrate_t(cg_context *c, void *send)
+{
+    auto &S = c->slab;
+    const int n = (int)c->n_owned;
+    const int64_t stay = S.h_counts[S.rank];
+    const int ndep = (int)(n - stay);
+    if (ndep == 0) return CG_OK;
+    cudaStream_t st = c->stream;
+    unsigned long long off[kMaxWorld];
+    unsigned long long acc = 0;
+    for (int k = 0; k < S.world; ++k) {
+        off[k] = acc;
+        if (k != S.rank) acc += (unsigned long long)S.h_counts[k];
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(S.dest_off, off, sizeof(unsigned long long) * S.world, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(c, cudaMemsetAsync(S.cursor, 0, sizeof(unsigned) * kMaxWorld, st));
+    CUDA_TRY(c, cudaMemsetAsync(S.cnt, 0, sizeof(unsigned) * 8, st));
+    const int n_keep = (int)stay;
+    slab_lists<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, n_keep, S.rank, S.dest, S.dep, S.holes, S.movers, S.cnt);
+    const SlabCols<T> C = cur_cols<T>(c);
+    slab_pack<T><<<cdiv(ndep, kThreads), kThreads, 0, st>>>(ndep, S.dep, S.dest, S.dest_off, S.cursor, C,
+                                                             (SlabRecord<T> *)send);
+    // |holes| = departures below n_keep <= ndep; the kernel reads the count on device
+    slab_fill_holes_dev<T><<<cdiv(ndep, kThreads), kThreads, 0, st>>>(S.cnt + 1, S.holes, S.movers, C);
+    LAUNCH_CHECK(c);
+    c->launches += 3;
+    CUDA_TRY(c, cudaStreamSynchronize(st));   // the send buffer is handed to the exchange
+    c->n = c->n_owned = n_keep;
+    c->bbox_valid = false;
+    return CG_OK;
+}
+
+template <typename T>
+static int slab_unpack_t(cg_context *c, const void *recv, int64_t count, bool ghosts)
+{
+    if (count <= 0) return CG_OK;
+    const int64_t base = ghosts ? c->n_owned : c->n_owned;
+    if (base + count > c->cap)
+        return fail(c, CG_ERR_POOL_CAPACITY, "slab needs %lld agents, capacity %lld (cg_reserve)",
+                    (long long)(base + count), (long long)c->cap);
+    cudaStream_t st = c->stream;
+    slab_unpack<T><<<cdiv(count, kThreads), kThreads, 0, st>>>((int)count, (int)base, (const SlabRecord<T> *)recv,
+                                                                cur_cols<T>(c), ghosts ? nullptr : c->maxd_enc);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    if (ghosts) {
+        c->n = base + count;
+    } else {
+        unsigned long long enc = 0;
+        CUDA_TRY(c, cudaMemcpyAsync(&enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        c->max_diam = dec_ordered(enc);
+        c->n = c->n_owned = base + count;
+        c->bbox_valid = false;
+    }
+    return CG_OK;
+}
+
+template <typename T>
+static int slab_halo_t(cg_context *c, void *send, int64_t counts[2])
+{
+    auto &S = c->slab;
+    cudaStream_t st = c->stream;
+    const int n = (int)c->n_owned;
+    if (!send) {
+        CUDA_TRY(c, cudaMemsetAsync(S.cnt, 0, sizeof(unsigned) * 8, st));
+        const int lo_plane = S.rank > 0 ? S.x0 : -2, hi_plane = S.rank < S.world - 1 ? S.x1 - 1 : -2;
+        if (n > 0) {
+            slab_halo_list<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, S.g, lo_plane, hi_plane,
+                                                                       (const T *)c->b.pos[c->cur_pos][0], S.lo,
+                                                                       S.hi, S.cnt);
+            LAUNCH_CHECK(c);
+            c->launches += 1;
+        }
+        CUDA_TRY(c, cudaMemcpyAsync(S.h_halo, S.cnt, sizeof(unsigned) * 2, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        counts[0] = S.h_halo[0];
+        counts[1] = S.h_halo[1];
+        return CG_OK;
+    }
+    const SlabCols<T> C = cur_cols<T>(c);
+    SlabRecord<T> *out = (SlabRecord<T> *)send;
+    if (S.h_halo[0])
+        slab_gather_records<T><<<cdiv(S.h_halo[0], kThreads), kThreads, 0, st>>>((int)S.h_halo[0], S.lo, C, out);
+    if (S.h_halo[1])
+        slab_gather_records<T><<<cdiv(S.h_halo[1], kThreads), kThreads, 0, st>>>((int)S.h_halo[1], S.hi, C,
+                                                                               out + S.h_halo[0]);
+    LAUNCH_CHECK(c);
+    c->launches += 2;
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    return CG_OK;
+}
+
+template <typename T>
+static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t *step_id)
+{
+    auto &S = c->slab;
+    if (!S.planned) return fail(c, CG_ERR_STATE, "cg_slab_step without cg_slab_plan");
+    const int slot = (int)(c->steps_done % kRing);
+    cg_step_stats &St = c->ring[slot];
+    std::memset(&St, 0, sizeof St);
+    St.step_id = c->steps_done;
+    St.agent_count = c->n_owned;
+    *step_id = c->steps_done;
+    cudaStream_t st = c->stream;
+    int rc;
+    // exact bbox of the owned set (the sweep's shell filter needs it)
+    if (!c->bbox_valid && c->n_owned > 0 && (rc = standalone_bbox<T>(c))) return rc;
+    // sub-grid: global planes [x0 - 1, x1 + 1) clipped to the grid
+    Geometry g = S.g;
+    const int xl = std::max(S.x0 - 1, 0), xh = std::min(S.x1 + 1, S.g.dimx);
+    g.xoff = xl;
+    g.gdimx = S.g.dimx;
+    g.dimx = std::max(xh - xl, 1);
+    g.nb = g.dimx * g.dimy * g.dimz;
+    const bool freeze = (flags & CG_STEP_FREEZE) != 0;
+    const bool record = (flags & CG_STEP_RECORD) != 0;
+    if (c->n > 0) {
+        if ((rc = build_grid_geo<T>(c, g, false, false))) return rc;
+        CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
+        if ((rc = run_sweep<T>(c, params, freeze, record))) return rc;
+        if (!freeze) c->cur_pos = 1 - c->cur_pos;
+    } else {
+        CUDA_TRY(c, cudaMemsetAsync(c->stat_dev + slot * kStatSlots, 0, sizeof(unsigned long long) * kStatSlots, st));
+        for (int e = 0; e < 3; ++e) CUDA_TRY(c, cudaEventRecord(c->ev[slot][e], st));
+        c->bbox_valid = false;
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][3], st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->stat_host + slot * kStatSlots, c->stat_dev + slot * kStatSlots,
+                                sizeof(unsigned long long) * kStatSlots, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][4], st));
+    St.grid_dims[0] = S.g.dimx;
+    St.grid_dims[1] = S.g.dimy;
+    St.grid_dims[2] = S.g.dimz;
+    St.origin[0] = S.g.ox;
+    St.origin[1] = S.g.oy;
+    St.origin[2] = S.g.oz;
+    St.box_length = S.g.L;
+    c->n = c->n_owned;   // this step's ghosts are dropped
+    c->last_record = record;
+    c->have_grid = false;   // the sub-grid is not exportable
+    c->pres_state = PRES_IDENTITY;
+    c->steps_done++;
+    S.planned = false;
     return CG_OK;
 }
 
@@ -830,6 +1086,8 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
         if (rc) return rc;
     }
     c->n = n;
+    c->n_owned = n;
+    c->slab.planned = false;
     c->cur_pos = c->cur_attr = 0;
     c->have_grid = false;
     c->relaid = false;
@@ -996,11 +1254,11 @@ int cg_box_ids(cg_context *c, int64_t n, const void *px, const void *py, const v
     CUDA_TRY(c, cudaSetDevice(c->device));
     int rc = CG_OK;
     if (n > c->cap && (rc = alloc_agents(c, n))) return rc;
-    c->n = 0;   // the resident pool is overwritten by this call
+    c->n = c->n_owned = 0;   // the resident pool is overwritten by this call
     c->have_grid = false;
     c->bbox_valid = false;
     c->pres_state = PRES_IDENTITY;
-    Geometry g{box_length, ox, oy, oz, (int)dimx, (int)dimy, (int)dimz, (int)(dimx * dimy * dimz)};
+    Geometry g{box_length, ox, oy, oz, (int)dimx, (int)dimy, (int)dimz, (int)(dimx * dimy * dimz), 0, (int)dimx};
     const size_t fe = c->esz * (size_t)n;
     const void *src[3] = {px, py, pz};
     for (int a = 0; a < 3; ++a)
@@ -1037,7 +1295,7 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     const int64_t nb64 = dimx * dimy * dimz;
     if (nb64 >= (int64_t)INT32_MAX / 2) return fail(c, CG_ERR_GRID_OVERFLOW, "too many boxes");
     if ((rc = ensure_boxes(c, nb64))) return rc;
-    Geometry g{1.0, 0.0, 0.0, 0.0, (int)dimx, (int)dimy, (int)dimz, (int)nb64};
+    Geometry g{1.0, 0.0, 0.0, 0.0, (int)dimx, (int)dimy, (int)dimz, (int)nb64, 0, (int)dimx};
     c->geo = g;
     c->bd = make_decode(g);
     const int nblk = cdiv(nn, kThreads);
@@ -1087,10 +1345,104 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     counters[0] = (int64_t)h[2];
     counters[1] = (int64_t)h[3];
     counters[2] = (int64_t)h[4];
-    c->n = 0;   // the resident buffers no longer hold a consistent pool
+    c->n = c->n_owned = 0;   // the resident buffers no longer hold a consistent pool
     c->have_grid = false;
     c->bbox_valid = false;
     return CG_OK;
 }
 
+int64_t cg_record_bytes(const cg_context *c)
+{
+    if (!c) return -1;
+    return (int64_t)(c->esz == 8 ? sizeof(SlabRecord<double>) : sizeof(SlabRecord<float>));
+}
+
+int cg_reserve(cg_context *c, int64_t capacity)
+{
+    if (!c) return CG_ERR_VALUE;
+    if (c->n > 0) return fail(c, CG_ERR_STATE, "cg_reserve must precede cg_upload");
+    if (capacity >= (int64_t)INT32_MAX / 4) return fail(c, CG_ERR_POOL_CAPACITY, "capacity too large");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (capacity > c->cap) return alloc_agents(c, capacity);
+    return CG_OK;
+}
+
+int cg_local_bbox(cg_context *c, double out[7])
+{
+    if (!c) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (c->n_owned == 0) {
+        out[0] = out[1] = out[2] = INFINITY;
+        out[3] = out[4] = out[5] = -INFINITY;
+        out[6] = c->max_diam;
+        return CG_OK;
+    }
+    int rc = CG_OK;
+    if (!c->bbox_valid)
+        rc = c->prec == CG_FP64 ? standalone_bbox<double>(c) : standalone_bbox<float>(c);
+    else
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (rc) return rc;
+    for (int k = 0; k < 6; ++k) out[k] = c->bbox_host[k];
+    out[6] = c->max_diam;
+    return CG_OK;
+}
+
+int cg_slab_plan(cg_context *c, const double bbox[7], double interaction_radius, int64_t box_cap, int world,
+                 int rank, int64_t *counts, int64_t planes[2])
+{
+    if (!c) return CG_ERR_VALUE;
+    if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world) return fail(c, CG_ERR_VALUE, "bad world/rank");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (c->n != c->n_owned) return fail(c, CG_ERR_STATE, "ghosts from an unfinished slab step");
+    return c->prec == CG_FP64 ? slab_plan_t<double>(c, bbox, interaction_radius, box_cap, world, rank, counts, planes)
+                              : slab_plan_t<float>(c, bbox, interaction_radius, box_cap, world, rank, counts, planes);
+}
+
+int cg_slab_migrate(cg_context *c, void *send)
+{
+    if (!c) return CG_ERR_VALUE;
+    if (!c->slab.planned) return fail(c, CG_ERR_STATE, "cg_slab_migrate without cg_slab_plan");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    return c->prec == CG_FP64 ? slab_migrate_t<double>(c, send) : slab_migrate_t<float>(c, send);
+}
+
+int cg_slab_accept(cg_context *c, const void *recv, int64_t count)
+{
+    if (!c) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    return c->prec == CG_FP64 ? slab_unpack_t<double>(c, recv, count, false)
+                              : slab_unpack_t<float>(c, recv, count, false);
+}
+
+int cg_slab_halo(cg_context *c, void *send, int64_t counts[2])
+{
+    if (!c) return CG_ERR_VALUE;
+    if (!c->slab.planned) return fail(c, CG_ERR_STATE, "cg_slab_halo without cg_slab_plan");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    return c->prec == CG_FP64 ? slab_halo_t<double>(c, send, counts) : slab_halo_t<float>(c, send, counts);
+}
+
+int cg_slab_set_ghosts(cg_context *c, const void *recv, int64_t count)
+{
+    if (!c) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    c->n = c->n_owned;
+    return c->prec == CG_FP64 ? slab_unpack_t<double>(c, recv, count, true)
+                              : slab_unpack_t<float>(c, recv, count, true);
+}
+
+int cg_slab_step(cg_context *c, const double params[5], int flags, cg_step_stats *stats)
+{
+    if (!c) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    int64_t id = -1;
+    const int rc = c->prec == CG_FP64 ? slab_step_t<double>(c, params, flags, &id)
+                                      : slab_step_t<float>(c, params, flags, &id);
+    if (rc) return rc;
+    if (stats) return collect(c, id, stats);
+    return CG_OK;
+}
+
 }  // extern "C"
+

@@ -204,7 +204,7 @@ __device__ __forceinline__ int axis_box(double p, double o, double L, int dim)
 template <typename T>
 __device__ __forceinline__ int flat_box(const Geometry &g, T x, T y, T z)
 {
-    const int ix = axis_box((double)x, g.ox, g.L, g.dimx);
+    const int ix = axis_box((double)x, g.ox, g.L, g.gdimx) - g.xoff;
     const int iy = axis_box((double)y, g.oy, g.L, g.dimy);
     const int iz = axis_box((double)z, g.oz, g.L, g.dimz);
     return (ix * g.dimy + iy) * g.dimz + iz;
@@ -425,7 +425,7 @@ template <typename T>
 __device__ __forceinline__ void put_proxy(const Proxies &P, const Geometry &g, int s, int ix, int iy, T x, T y, T z)
 {
     const int q = s >> 1, h = s & 1;
-    P.xy[4 * q + h] = (float)((double)x - (g.ox + (double)ix * g.L));
+    P.xy[4 * q + h] = (float)((double)x - (g.ox + (double)(ix + g.xoff) * g.L));
     P.xy[4 * q + 2 + h] = (float)((double)y - (g.oy + (double)iy * g.L));
     P.z[s] = (float)((double)z - g.oz);
 }

@@ -56,6 +56,7 @@ struct Sweep7Args {
     double shell_lo[3], shell_hi[3];   // bbox shell: old lo + max move, old hi - max move
     int *ovf;                   // slots of agents deferred to the overflow kernel
     unsigned *ovf_count;
+    int n_owned;                // storage indices >= n_owned are ghosts (slab halo): not targets
 };
 
 // packed fp32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2)
@@ -108,6 +109,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         int ix, iy, iz;
         decode_box(A.bd, key, ix, iy, iz);
         const int a = A.idx ? __ldg(A.idx + s) : s;
+        if (a >= A.n_owned) return;   // a ghost: candidate only
         const T half = T(0.5), zero = A.p.zero;
         const float mex = __ldg(A.prox.xy + 4 * (s >> 1) + (s & 1));
         const float mey = __ldg(A.prox.xy + 4 * (s >> 1) + 2 + (s & 1));

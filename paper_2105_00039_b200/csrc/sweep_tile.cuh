@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 3) sweep_tile_kernel(Sweep7Args<T> A
     const int ncols = HX * HY;
     const int BW = HZ + 1;                // box offsets per column run
     // tile centre (frame of the fp32 proxies)
-    const double ccx = A.g.ox + 0.5 * (double)(cx0 + cx1) * A.g.L;
+    const double ccx = A.g.ox + 0.5 * (double)(cx0 + cx1 + 2 * A.g.xoff) * A.g.L;
     const double ccy = A.g.oy + 0.5 * (double)(cy0 + cy1) * A.g.L;
     const double ccz = A.g.oz + 0.5 * (double)(cz0 + cz1) * A.g.L;
 
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 3) sweep_tile_kernel(Sweep7Args<T> A
         const int base = ((hx0 + lx) * A.g.dimy + (hy0 + ly)) * A.g.dimz + hz0;
         boff[q] = __ldg(A.off + base + zz);
     }
-    if (threadIdx.x <= HX) xlo[threadIdx.x] = (float)(A.g.ox + (double)(hx0 + (int)threadIdx.x) * A.g.L - ccx);
+    if (threadIdx.x <= HX) xlo[threadIdx.x] = (float)(A.g.ox + (double)(hx0 + A.g.xoff + (int)threadIdx.x) * A.g.L - ccx);
     if (threadIdx.x >= 32 && threadIdx.x - 32 <= HY)
         ylo[threadIdx.x - 32] = (float)(A.g.oy + (double)(hy0 + (int)threadIdx.x - 32) * A.g.L - ccy);
     __syncthreads();
@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 3) sweep_tile_kernel(Sweep7Args<T> A
             continue;
         }
         const int a = A.idx ? __ldg(A.idx + s) : s;
+        if (a >= A.n_owned) continue;   // a ghost: candidate only
         const int lz = bz[e];
         const float mex = xs[e], mey = ys[e], mez = zs[e];
         const T half = T(0.5), zero = A.p.zero;
