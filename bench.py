@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "gloo"],
+                    help="multi-GPU exchange (gloo: host-staged, e.g. several ranks on one GPU)")
+    ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (testing)")
     return ap.parse_args()
 
 
@@ -174,15 +177,20 @@ def cpu_port_run(pool, precision, steps, sort_every, freeze):
     return float(np.median(ts)), th
 
 
-def dist_init():
+def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.exchange == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return rank, world, local
 
 
@@ -191,7 +199,8 @@ def reduce_max(v, world):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -225,11 +234,115 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def main_slab(args, rank, world, local):
+    """N > 1: C5 weak scaling -- each rank starts with its 256-plane x-slab of the
+    (256 G) x 256 x 256 jittered lattice; x-slab decomposition with halo
+    exchange and migration every step (paper_2105_00039_b200/distributed.py)."""
+    import torch
+    from paper_2105_00039_b200 import _native
+    from paper_2105_00039_b200.distributed import SlabRunner, TorchExchange
+    torch.cuda.set_device(local)
+    pool, desc = make_pool(args.config, args.precision, rank, world)
+    n0 = pool.count
+    ctx = _native.Context(local, pool.dtype)
+    ctx.set_option(_native.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[args.summation])
+    ctx.reserve(int(n0 * 1.05) + 4 * 256 * 256 * 2 + 4096)
+    ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+    ex = TorchExchange(device="cuda", device_buffers=args.exchange == "nccl")
+    runner = SlabRunner(ctx, ex)
+    params = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
+    flags = _native.CG_STEP_FREEZE if args.freeze else 0
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            runner.step(params, flags)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        launches0 = ctx.launches
+        barrier(world)
+        torch.cuda.synchronize()
+        with Clocks(local) as clk:
+            ev0.record(stream)
+            stats = [runner.step(params, flags) for _ in range(args.steps)]
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        launches = ctx.launches - launches0
+        barrier(world)
+    ms = reduce_max(ev0.elapsed_time(ev1) / args.steps, world)
+    total = stats[-1].agents
+    value = total / (ms * 1e-3)
+    t_force = float(np.mean([ctx.fetch_stats(ctx.steps - 1 - k).t_force_ms for k in range(min(args.steps, 8))]))
+    t_force = reduce_max(t_force, world)
+    n_local = ctx.n
+    # e2e: each rank's shard crosses the host boundary every step (pinned
+    # host -> device upload, slab step, device -> pinned host download)
+    e2e = None
+    if args.e2e_steps > 0:
+        import time as _t
+        cap = int(n0 * 1.05) + 4 * 256 * 256 * 2 + 4096
+        pin = {k: _native.PinnedArray.empty(cap, np.uint64 if k == "uid" else pool.dtype)
+               for k in ("px", "py", "pz", "diameter", "adherence", "uid", "dx", "dy", "dz")}
+        cols = ctx.download()
+        n = ctx.n
+        for k in pin:
+            pin[k][:n] = cols[k]
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        h2d = d2h = 0
+        with torch.cuda.stream(stream):
+            for _ in range(args.e2e_steps):
+                ctx.upload(pin["px"][:n], pin["py"][:n], pin["pz"][:n], pin["diameter"][:n],
+                           pin["adherence"][:n], pin["uid"][:n])
+                h2d += n * (5 * np.dtype(pool.dtype).itemsize + 8)
+                runner.step(params, flags)
+                n = ctx.n
+                ctx.download(into={k: v[:n] for k, v in pin.items()})
+                d2h += n * (8 * np.dtype(pool.dtype).itemsize + 8)
+        torch.cuda.synchronize()
+        t_e2e = reduce_max((_t.perf_counter() - t0) / args.e2e_steps, world)
+        e2e = {"value": total / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.e2e_steps,
+               "d2h_bytes_per_step": d2h // args.e2e_steps, "ms_per_step": t_e2e * 1e3,
+               "scope": "rank 0's bytes; every rank moves its own shard",
+               "api": "distributed.SlabRunner.step between cg_upload / cg_download of the shard"}
+    ctx.close()
+    if rank != 0:
+        return
+    peak, peak_src = measured_hbm_peak()
+    bal = B_ALG[args.precision]
+    achieved = n_local * bal / (t_force * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": "C5: (256 x %d) x 256 x 256 jittered lattice, %d agents (%d per GPU at start)"
+                               % (world, total, n0),
+                   "agents_total": total, "summation": args.summation, "freeze": args.freeze,
+                   "l2": "inputs larger than L2 (%.0f MB of agent state per GPU)" % (n0 * 64 / 1e6),
+                   "parallelism": "x-slabs x%d, %s halo exchange + migration every step" % (world, args.exchange)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "sweep7_kernel (per GPU)",
+                     "alg_bytes_per_agent": bal, "kernel_ms": t_force, "peak_source": peak_src},
+        "step_roofline_frac": total / world * bal / (ms * 1e-3) / 1e9 / peak,
+        "pair_interactions_per_s": stats[-1].force_evals / (ms * 1e-3),
+        "candidates_per_s": stats[-1].candidates / (ms * 1e-3),
+        "migrated_last_step": stats[-1].migrated_in, "ghosts_last_step": stats[-1].ghosts,
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "cpu_baseline": None,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
-    rank, world, local = dist_init()
+    rank, world, local = dist_init(args)
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if world > 1:
+        main_slab(args, rank, world, local)
         return
     import torch
     from paper_2105_00039_b200 import _native

@@ -775,7 +775,9 @@ static int slab_plan_t(cg_context *c, const double bb[7], double ir, int64_t box
     Geometry g;
     int64_t dims64[3];
     double origin[3];
-    if ((rc = host_geometry(c, bb, ir, box_cap, g, dims64, origin))) return rc;
+    // the box cap bounds each rank's sub-grid (the reference's cap is a
+    // per-process memory bound, spatial.py:111-116)
+    if ((rc = host_geometry(c, bb, ir, INT64_MAX, g, dims64, origin))) return rc;
     if (g.dimx < world)
         return fail(c, CG_ERR_VALUE, "grid of %d x-planes is too narrow for %d slabs", g.dimx, world);
     S.g = g;
@@ -785,6 +787,12 @@ static int slab_plan_t(cg_context *c, const double bb[7], double ir, int64_t box
     for (int k = 0; k <= world; ++k) S.B.x[k] = (int)(((int64_t)k * g.dimx) / world);
     S.x0 = S.B.x[rank];
     S.x1 = S.B.x[rank + 1];
+    {
+        const int64_t sub = (int64_t)(std::min(S.x1 + 1, g.dimx) - std::max(S.x0 - 1, 0)) * g.dimy * g.dimz;
+        if (sub > box_cap)
+            return fail(c, CG_ERR_GRID_OVERFLOW, "slab sub-grid of %lld boxes exceeds cap %lld",
+                        (long long)sub, (long long)box_cap);
+    }
     planes[0] = S.x0;
     planes[1] = S.x1;
     cudaStream_t st = c->stream;
