@@ -52,8 +52,7 @@ extern "C" {
 
 /* cg_set_option keys */
 #define CG_OPT_SUMMATION 1      /* 0 = uid order (bit-exact vs reference), 1 = stencil order */
-#define CG_OPT_SWEEP 3          /* 0 = reference-order thread-per-agent sweep, 1 = production sweep (default),
-                                   2 = shared-memory tiles for sparse pools */
+#define CG_OPT_SWEEP 3          /* 0 = reference-order thread-per-agent sweep, 1 = production sweep (default) */
 #define CG_OPT_RELAYOUT_EVERY 4 /* move the records into slot order on every k-th sort step (k >= 1, default 1) */
 #define CG_OPT_PATH 5           /* 0 = auto (by agents per box), 1 = sparse (uid-sorted survivor lists),
                                    2 = dense (boxes ordered by (z, uid), CG_OPT_SUMMATION applies) */

@@ -35,7 +35,6 @@
 #include "grid.cuh"
 #include "sweep.cuh"
 #include "sweep7.cuh"
-#include "sweep_tile.cuh"
 #include "slab.cuh"
 
 using namespace cg;
@@ -50,8 +49,7 @@ constexpr int kMaxCounterBlocks = 1 << 20;
 enum { PRES_IDENTITY = 0, PRES_VALID = 1, PRES_PENDING = 2 };
 
 struct Buffers {
-    void *pos[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-    void *dia[2] = {nullptr, nullptr};
+    void *rec[2] = {nullptr, nullptr};   // Rec<T>: x, y, z, diameter (double-buffered)
     void *adh[2] = {nullptr, nullptr};
     uint64_t *uid[2] = {nullptr, nullptr};
     void *disp[3] = {nullptr, nullptr, nullptr};
@@ -110,7 +108,7 @@ struct cg_context {
     Geometry geo_sort{};          // geometry of the last sort step (presentation order)
     // options
     int summation = SUM_UID;
-    int sweep_impl = 1;           // 0 = reference-order thread per agent, 1 = sweep7, 2 = smem tiles (sparse)
+    int sweep_impl = 1;           // 0 = reference-order thread per agent, 1 = sweep7 (production)
     int relayout_every = 1;       // relayout on every k-th sort step (1 = every sort step)
     int path = 0;                 // 0 = auto, 1 = sparse (uid-sorted lists), 2 = dense (z-sorted boxes)
     // x-slab decomposition (multi-GPU)
@@ -156,8 +154,7 @@ static int fail(cg_context *c, int code, const char *fmt, ...)
 static void free_agents(cg_context *c)
 {
     Buffers &b = c->b;
-    void *ptrs[] = {b.pos[0][0], b.pos[0][1], b.pos[0][2], b.pos[1][0], b.pos[1][1], b.pos[1][2],
-                    b.dia[0], b.dia[1], b.adh[0], b.adh[1], b.uid[0], b.uid[1],
+    void *ptrs[] = {b.rec[0], b.rec[1], b.adh[0], b.adh[1], b.uid[0], b.uid[1],
                     b.disp[0], b.disp[1], b.disp[2], b.key_rank, b.tmp, b.idx, b.skey, b.pres,
                     b.rec_m, b.rec_nk, b.prox, b.stage, b.pkey[0], b.pkey[1], b.pscratch, b.ovf};
     for (void *p : ptrs)
@@ -172,8 +169,7 @@ static int alloc_agents(cg_context *c, int64_t cap)
     Buffers &b = c->b;
     const size_t fe = c->esz * (size_t)cap, ie = sizeof(int) * (size_t)cap;
     for (int k = 0; k < 2; ++k) {
-        for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMalloc(&b.pos[k][a], fe));
-        CUDA_TRY(c, cudaMalloc(&b.dia[k], fe));
+        CUDA_TRY(c, cudaMalloc(&b.rec[k], 4 * fe));
         CUDA_TRY(c, cudaMalloc(&b.adh[k], fe));
         CUDA_TRY(c, cudaMalloc(&b.uid[k], sizeof(uint64_t) * (size_t)cap));
     }
@@ -295,8 +291,8 @@ static int standalone_bbox(cg_context *c)
 {
     const int n = (int)c->n_owned;
     cudaStream_t st = c->stream;
-    T *x = (T *)c->b.pos[c->cur_pos][0], *y = (T *)c->b.pos[c->cur_pos][1], *z = (T *)c->b.pos[c->cur_pos][2];
-    bbox_slots<T><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(n, x, y, z, c->slots);
+    bbox_slots<T><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(
+        n, (const Rec<T> *)c->b.rec[c->cur_pos], c->slots);
     finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, nullptr, c->bbox_dev, FINISH_BBOX);
     LAUNCH_CHECK(c);
     c->launches += 2;
@@ -398,8 +394,8 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
     unsigned long long *stat = c->stat_dev + slot * kStatSlots;
     CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
     const int nblk = cdiv(n, kThreads);
-    T *x = (T *)c->b.pos[c->cur_pos][0], *y = (T *)c->b.pos[c->cur_pos][1], *z = (T *)c->b.pos[c->cur_pos][2];
-    box_keys<T><<<nblk, kThreads, 0, st>>>(n, g, x, y, z, c->count, c->b.key_rank);
+    const Rec<T> *rec = (const Rec<T> *)c->b.rec[c->cur_pos];
+    box_keys<T><<<nblk, kThreads, 0, st>>>(n, g, rec, c->count, c->b.key_rank);
     LAUNCH_CHECK(c);
     c->launches += 1;
     if ((rc = launch_scan(c, false, g.nb, c->offset, stat))) return rc;
@@ -410,15 +406,14 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
     const int a = c->cur_attr, o = 1 - c->cur_pos, oa = 1 - c->cur_attr;
     int *pk = sort ? c->b.pkey[a] : nullptr;
     if (!dense) {
-        place_full<T><<<nblk, kThreads, 0, st>>>(n, g, c->bd, c->b.key_rank, c->offset, x, y, z, c->b.idx,
+        place_full<T><<<nblk, kThreads, 0, st>>>(n, g, c->bd, c->b.key_rank, c->offset, rec, c->b.idx,
                                                  c->b.skey, c->b.P(), pk);
         LAUNCH_CHECK(c);
         c->launches += 1;
         CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
         if (relayout) {
             relayout_records<T><<<nblk, kThreads, 0, st>>>(
-                n, c->b.idx, x, y, z, (T *)c->b.dia[a], (T *)c->b.adh[a], c->b.uid[a], pk,
-                (T *)c->b.pos[o][0], (T *)c->b.pos[o][1], (T *)c->b.pos[o][2], (T *)c->b.dia[oa],
+                n, c->b.idx, rec, (T *)c->b.adh[a], c->b.uid[a], pk, (Rec<T> *)c->b.rec[o],
                 (T *)c->b.adh[oa], c->b.uid[oa], c->b.pkey[oa]);
             LAUNCH_CHECK(c);
             c->launches += 1;
@@ -430,15 +425,13 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
         CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
         if (relayout) {
             order_gather<T, true><<<nblk, kThreads, 0, st>>>(
-                n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, x, y, z, (T *)c->b.dia[a],
-                (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(), nullptr, (T *)c->b.pos[o][0],
-                (T *)c->b.pos[o][1], (T *)c->b.pos[o][2], (T *)c->b.dia[oa], (T *)c->b.adh[oa], c->b.uid[oa],
+                n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, rec, (T *)c->b.adh[a], c->b.uid[a],
+                c->b.skey, c->b.P(), nullptr, (Rec<T> *)c->b.rec[o], (T *)c->b.adh[oa], c->b.uid[oa],
                 sort ? c->b.pkey[oa] : nullptr);
         } else {
             order_gather<T, false><<<nblk, kThreads, 0, st>>>(
-                n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, x, y, z, (T *)c->b.dia[a],
-                (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr, nullptr,
-                nullptr, nullptr, nullptr, pk);
+                n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, rec, (T *)c->b.adh[a], c->b.uid[a],
+                c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr, nullptr, pk);
         }
         LAUNCH_CHECK(c);
         c->launches += 1;
@@ -472,49 +465,13 @@ static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
     return CG_OK;
 }
 
-// Tile shape of the sparse-path sweep: 4 x 4 columns x TZ boxes with about
-// 240 core agents; staging capacity 1.25x the expected halo population.
-static TileCfg choose_tile(const Geometry &g, int64_t n)
-{
-    const double rho = (double)n / (double)g.nb;
-    TileCfg C;
-    C.tx = std::min(4, g.dimx);
-    C.ty = std::min(4, g.dimy);
-    C.tz = (int)std::lround(240.0 / (C.tx * C.ty * std::max(rho, 1e-3)));
-    C.tz = std::max(1, std::min(C.tz, std::min(64, g.dimz)));
-    C.ntx = cdiv(g.dimx, C.tx);
-    C.nty = cdiv(g.dimy, C.ty);
-    C.ntz = cdiv(g.dimz, C.tz);
-    C.max_cols = (C.tx + 2) * (C.ty + 2);
-    const double halo = (double)C.max_cols * (C.tz + 2) * rho;
-    C.cap = ((int)(1.25 * halo + 96.0) + 1) & ~1;
-    const double E = g.L * (double)std::max(C.tx + 2, std::max(C.ty + 2, C.tz + 2));
-    C.margin = (float)(64.0 * E * 5.9604644775390625e-8);
-    return C;
-}
-
 template <typename T>
 static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
 {
     if (!c->last_dense) {
-        // sparse: shared-memory tiles, survivors summed in uid order (deterministic
-        // and bit-identical to the reference whatever the slot order in a box);
-        // agents with many survivors / tiles over capacity go to the overflow kernel
-        cudaStream_t st = c->stream;
-        const TileCfg C = choose_tile(c->geo, c->n);
-        const size_t sm = TileLayout<T>(C.cap, C.max_cols, C.tz).total;
-        const long long ntiles = (long long)C.ntx * C.nty * C.ntz;
-        if (c->sweep_impl == 2 && sm <= 160 * 1024 && ntiles < INT32_MAX) {
-            auto k = sweep_tile_kernel<T, 16>;
-            CUDA_TRY(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
-            k<<<(int)ntiles, kThreads, sm, st>>>(A, C);
-            LAUNCH_CHECK(c);
-            sweep7_overflow<T, true, false, 16><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
-            LAUNCH_CHECK(c);
-            c->launches += 2;
-            return CG_OK;
-        }
+        // sparse: survivors summed in uid order (deterministic and bit-identical to
+        // the reference whatever the slot order in a box); agents with more than
+        // 16 survivors go to the overflow kernel
         return launch_sweep7_k<T, true, false, 16, false, 4>(c, A);
     }
     if (c->summation == SUM_UID) return launch_sweep7_k<T, true, true, 16, false, 3>(c, A);
@@ -528,9 +485,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     const int n = (int)c->n;
     cudaStream_t st = c->stream;
     const int cp = c->cur_pos, ca = c->cur_attr;
-    T *nx = freeze ? nullptr : (T *)c->b.pos[1 - cp][0];
-    T *ny = freeze ? nullptr : (T *)c->b.pos[1 - cp][1];
-    T *nz = freeze ? nullptr : (T *)c->b.pos[1 - cp][2];
+    Rec<T> *nrec = freeze ? nullptr : (Rec<T> *)c->b.rec[1 - cp];
     const Params<T> P = make_params<T>(params);
     if (c->sweep_impl == 0) {
         // reference-order thread-per-agent sweep (sweep.cuh), then a standalone bbox next step
@@ -539,10 +494,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
         SweepArgs<T> A{};
         A.n = n;
         A.g = c->geo;
-        A.x = (const T *)c->b.pos[cp][0];
-        A.y = (const T *)c->b.pos[cp][1];
-        A.z = (const T *)c->b.pos[cp][2];
-        A.d = (const T *)c->b.dia[ca];
+        A.rec = (const Rec<T> *)c->b.rec[cp];
         A.adh = (const T *)c->b.adh[ca];
         A.uid = c->b.uid[ca];
         A.idx = c->relaid ? nullptr : c->b.idx;
@@ -552,9 +504,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
         A.disp_x = (T *)c->b.disp[0];
         A.disp_y = (T *)c->b.disp[1];
         A.disp_z = (T *)c->b.disp[2];
-        A.new_x = nx;
-        A.new_y = ny;
-        A.new_z = nz;
+        A.new_rec = nrec;
         A.rec_m = record ? c->b.rec_m : nullptr;
         A.rec_nk = record ? c->b.rec_nk : nullptr;
         A.block_counters = c->block_counters;
@@ -581,10 +531,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     A.skey = c->b.skey;
     A.idx = c->relaid ? nullptr : c->b.idx;
     A.off = c->offset;
-    A.x = (const T *)c->b.pos[cp][0];
-    A.y = (const T *)c->b.pos[cp][1];
-    A.z = (const T *)c->b.pos[cp][2];
-    A.d = (const T *)c->b.dia[ca];
+    A.rec = (const Rec<T> *)c->b.rec[cp];
     A.adh = (const T *)c->b.adh[ca];
     A.uid = c->b.uid[ca];
     A.p = P;
@@ -596,9 +543,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     A.disp_x = (T *)c->b.disp[0];
     A.disp_y = (T *)c->b.disp[1];
     A.disp_z = (T *)c->b.disp[2];
-    A.new_x = nx;
-    A.new_y = ny;
-    A.new_z = nz;
+    A.new_rec = nrec;
     A.rec_m = record ? c->b.rec_m : nullptr;
     A.rec_nk = record ? c->b.rec_nk : nullptr;
     A.slots = c->slots;
@@ -753,10 +698,7 @@ template <typename T>
 static SlabCols<T> cur_cols(cg_context *c)
 {
     SlabCols<T> C;
-    C.x = (T *)c->b.pos[c->cur_pos][0];
-    C.y = (T *)c->b.pos[c->cur_pos][1];
-    C.z = (T *)c->b.pos[c->cur_pos][2];
-    C.d = (T *)c->b.dia[c->cur_attr];
+    C.rec = (Rec<T> *)c->b.rec[c->cur_pos];
     C.adh = (T *)c->b.adh[c->cur_attr];
     C.uid = c->b.uid[c->cur_attr];
     C.dx = (T *)c->b.disp[0];
@@ -799,7 +741,7 @@ static int slab_plan_t(cg_context *c, const double bb[7], double ir, int64_t box
     CUDA_TRY(c, cudaMemsetAsync(S.counts, 0, sizeof(unsigned long long) * kMaxWorld, st));
     const int n = (int)c->n_owned;
     if (n > 0) {
-        slab_dest<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, g, S.B, (const T *)c->b.pos[c->cur_pos][0], S.dest,
+        slab_dest<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, g, S.B, (const Rec<T> *)c->b.rec[c->cur_pos], S.dest,
                                                               S.counts);
         LAUNCH_CHECK(c);
         c->launches += 1;
@@ -882,7 +824,7 @@ static int slab_halo_t(cg_context *c, void *send, int64_t counts[2])
         const int lo_plane = S.rank > 0 ? S.x0 : -2, hi_plane = S.rank < S.world - 1 ? S.x1 - 1 : -2;
         if (n > 0) {
             slab_halo_list<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, S.g, lo_plane, hi_plane,
-                                                                       (const T *)c->b.pos[c->cur_pos][0], S.lo,
+                                                                       (const Rec<T> *)c->b.rec[c->cur_pos], S.lo,
                                                                        S.hi, S.cnt);
             LAUNCH_CHECK(c);
             c->launches += 1;
@@ -1066,7 +1008,7 @@ int cg_set_option(cg_context *c, int key, int value)
         c->summation = value;
         return CG_OK;
     }
-    if (key == CG_OPT_SWEEP && value >= 0 && value <= 2) {
+    if (key == CG_OPT_SWEEP && value >= 0 && value <= 1) {
         c->sweep_impl = value;
         return CG_OK;
     }
@@ -1105,22 +1047,33 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
     if (n == 0) return CG_OK;
     const size_t fe = c->esz * (size_t)n;
     cudaStream_t st = c->stream;
-    const void *src[3] = {px, py, pz};
-    for (int a = 0; a < 3; ++a)
-        CUDA_TRY(c, cudaMemcpyAsync(c->b.pos[0][a], src[a], fe, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(c, cudaMemcpyAsync(c->b.dia[0], diameter, fe, cudaMemcpyHostToDevice, st));
+    // SoA columns land in scratch (the displacement columns and the staging
+    // buffer) and are packed into records
+    const void *src[4] = {px, py, pz, diameter};
+    void *tmp4[4] = {c->b.disp[0], c->b.disp[1], c->b.disp[2], c->b.stage};
+    for (int a = 0; a < 4; ++a)
+        CUDA_TRY(c, cudaMemcpyAsync(tmp4[a], src[a], fe, cudaMemcpyHostToDevice, st));
     CUDA_TRY(c, cudaMemcpyAsync(c->b.adh[0], adherence, fe, cudaMemcpyHostToDevice, st));
     CUDA_TRY(c, cudaMemcpyAsync(c->b.uid[0], uid, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, st));
+    const int nblk = cdiv(n, kThreads);
+    if (c->prec == CG_FP64)
+        pack_records<double><<<nblk, kThreads, 0, st>>>((int)n, (const double *)tmp4[0], (const double *)tmp4[1],
+                                                        (const double *)tmp4[2], (const double *)tmp4[3],
+                                                        (Rec<double> *)c->b.rec[0]);
+    else
+        pack_records<float><<<nblk, kThreads, 0, st>>>((int)n, (const float *)tmp4[0], (const float *)tmp4[1],
+                                                       (const float *)tmp4[2], (const float *)tmp4[3],
+                                                       (Rec<float> *)c->b.rec[0]);
     for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMemsetAsync(c->b.disp[a], 0, fe, st));
     CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, sizeof(unsigned long long), st));
     if (c->prec == CG_FP64)
-        max_diam_kernel<double><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(
-            (int)n, (const double *)c->b.dia[0], c->maxd_enc);
+        max_diam_kernel<double><<<std::min(kBboxBlocks, nblk), kThreads, 0, st>>>(
+            (int)n, (const Rec<double> *)c->b.rec[0], c->maxd_enc);
     else
-        max_diam_kernel<float><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(
-            (int)n, (const float *)c->b.dia[0], c->maxd_enc);
+        max_diam_kernel<float><<<std::min(kBboxBlocks, nblk), kThreads, 0, st>>>(
+            (int)n, (const Rec<float> *)c->b.rec[0], c->maxd_enc);
     LAUNCH_CHECK(c);
-    c->launches += 1;
+    c->launches += 2;
     unsigned long long enc = 0;
     CUDA_TRY(c, cudaMemcpyAsync(&enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));   // host buffers are only borrowed
@@ -1138,14 +1091,27 @@ int cg_download(cg_context *c, void *px, void *py, void *pz, void *diameter, voi
     int rc = materialize_presentation(c);
     if (rc) return rc;
     void *dst[9] = {px, py, pz, diameter, adherence, uid, dx, dy, dz};
-    const void *src[9] = {c->b.pos[c->cur_pos][0], c->b.pos[c->cur_pos][1], c->b.pos[c->cur_pos][2],
-                          c->b.dia[c->cur_attr], c->b.adh[c->cur_attr], c->b.uid[c->cur_attr],
+    const void *src[9] = {nullptr, nullptr, nullptr, nullptr, c->b.adh[c->cur_attr], c->b.uid[c->cur_attr],
                           c->b.disp[0], c->b.disp[1], c->b.disp[2]};
+    cudaStream_t st = c->stream;
+    const int *pres = c->pres_state == PRES_IDENTITY ? nullptr : c->b.pres;
     for (int k = 0; k < 9; ++k) {
         if (!dst[k]) continue;
-        if ((rc = download_column(c, src[k], dst[k], k == 5 ? 8 : c->esz))) return rc;
-        if (c->pres_state != PRES_IDENTITY)   // the staging buffer is reused per column
-            CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        if (k < 4) {   // record components, in the reference's order, through the staging buffer
+            if (c->prec == CG_FP64)
+                unpack_component<double><<<cdiv(n, kThreads), kThreads, 0, st>>>(
+                    (int)n, (const Rec<double> *)c->b.rec[c->cur_pos], k, pres, (double *)c->b.stage);
+            else
+                unpack_component<float><<<cdiv(n, kThreads), kThreads, 0, st>>>(
+                    (int)n, (const Rec<float> *)c->b.rec[c->cur_pos], k, pres, (float *)c->b.stage);
+            LAUNCH_CHECK(c);
+            c->launches += 1;
+            CUDA_TRY(c, cudaMemcpyAsync(dst[k], c->b.stage, c->esz * n, cudaMemcpyDeviceToHost, st));
+        } else if ((rc = download_column(c, src[k], dst[k], k == 5 ? 8 : c->esz))) {
+            return rc;
+        }
+        if (k < 4 || c->pres_state != PRES_IDENTITY)   // the staging buffer is reused per column
+            CUDA_TRY(c, cudaStreamSynchronize(st));
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return CG_OK;
@@ -1269,15 +1235,15 @@ int cg_box_ids(cg_context *c, int64_t n, const void *px, const void *py, const v
     Geometry g{box_length, ox, oy, oz, (int)dimx, (int)dimy, (int)dimz, (int)(dimx * dimy * dimz), 0, (int)dimx};
     const size_t fe = c->esz * (size_t)n;
     const void *src[3] = {px, py, pz};
-    for (int a = 0; a < 3; ++a)
-        CUDA_TRY(c, cudaMemcpyAsync(c->b.pos[0][a], src[a], fe, cudaMemcpyHostToDevice, c->stream));
+    for (int a = 0; a < 3; ++a)   // the displacement columns serve as scratch
+        CUDA_TRY(c, cudaMemcpyAsync(c->b.disp[a], src[a], fe, cudaMemcpyHostToDevice, c->stream));
     long long *dout = (long long *)c->b.stage;
     if (c->prec == CG_FP64)
         box_ids_only<double><<<cdiv(n, kThreads), kThreads, 0, c->stream>>>(
-            (int)n, g, (double *)c->b.pos[0][0], (double *)c->b.pos[0][1], (double *)c->b.pos[0][2], dout);
+            (int)n, g, (double *)c->b.disp[0], (double *)c->b.disp[1], (double *)c->b.disp[2], dout);
     else
         box_ids_only<float><<<cdiv(n, kThreads), kThreads, 0, c->stream>>>(
-            (int)n, g, (float *)c->b.pos[0][0], (float *)c->b.pos[0][1], (float *)c->b.pos[0][2], dout);
+            (int)n, g, (float *)c->b.disp[0], (float *)c->b.disp[1], (float *)c->b.disp[2], dout);
     LAUNCH_CHECK(c);
     c->launches += 1;
     CUDA_TRY(c, cudaMemcpyAsync(out, dout, sizeof(long long) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -1308,8 +1274,9 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     c->bd = make_decode(g);
     const int nblk = cdiv(nn, kThreads);
     if (nblk > kMaxCounterBlocks) return fail(c, CG_ERR_VALUE, "population too large");
-    if (c->prec == CG_FP64) double_column<double><<<nblk, kThreads, 0, st>>>(nn, (double *)c->b.dia[0]);
-    else double_column<float><<<nblk, kThreads, 0, st>>>(nn, (float *)c->b.dia[0]);
+    // radii were uploaded in the diameter slot: double them (exact)
+    if (c->prec == CG_FP64) double_diameter<double><<<nblk, kThreads, 0, st>>>(nn, (Rec<double> *)c->b.rec[0]);
+    else double_diameter<float><<<nblk, kThreads, 0, st>>>(nn, (Rec<float> *)c->b.rec[0]);
     long long *dbox = (long long *)c->b.stage;
     CUDA_TRY(c, cudaMemcpyAsync(dbox, box_index, sizeof(long long) * n, cudaMemcpyHostToDevice, st));
     keys_from_flat<<<nblk, kThreads, 0, st>>>(nn, dbox, c->count, c->b.key_rank);
@@ -1321,16 +1288,12 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     place<<<nblk, kThreads, 0, st>>>(nn, c->b.key_rank, c->offset, c->b.tmp);
     if (c->prec == CG_FP64)
         order_gather<double, false><<<nblk, kThreads, 0, st>>>(
-            nn, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, (double *)c->b.pos[0][0],
-            (double *)c->b.pos[0][1], (double *)c->b.pos[0][2], (double *)c->b.dia[0],
-            (double *)c->b.adh[0], c->b.uid[0], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr,
-            nullptr, nullptr, nullptr, nullptr, nullptr);
+            nn, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, (const Rec<double> *)c->b.rec[0],
+            (double *)c->b.adh[0], c->b.uid[0], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr, nullptr, nullptr);
     else
         order_gather<float, false><<<nblk, kThreads, 0, st>>>(
-            nn, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, (float *)c->b.pos[0][0],
-            (float *)c->b.pos[0][1], (float *)c->b.pos[0][2], (float *)c->b.dia[0],
-            (float *)c->b.adh[0], c->b.uid[0], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr,
-            nullptr, nullptr, nullptr, nullptr, nullptr);
+            nn, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, (const Rec<float> *)c->b.rec[0],
+            (float *)c->b.adh[0], c->b.uid[0], c->b.skey, c->b.P(), c->b.idx, nullptr, nullptr, nullptr, nullptr);
     LAUNCH_CHECK(c);
     c->launches += 5;
     c->relaid = false;

@@ -100,14 +100,14 @@ __global__ void init_slots(unsigned long long *__restrict__ slots)
 // relayout-free first step); in steady state the sweep epilogue produces the
 // same slots from the new positions.
 template <typename T>
-__global__ void __launch_bounds__(kThreads) bbox_slots(int n, const T *__restrict__ x, const T *__restrict__ y,
-                                                       const T *__restrict__ z,
+__global__ void __launch_bounds__(kThreads) bbox_slots(int n, const Rec<T> *__restrict__ rec,
                                                        unsigned long long *__restrict__ slots)
 {
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     unsigned long long c[3] = {0, 0, 0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const double p[3] = {(double)x[i], (double)y[i], (double)z[i]};
+        const Rec<T> r = rec[i];
+        const double p[3] = {(double)r.x, (double)r.y, (double)r.z};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             lo[a] = fmin(lo[a], p[a]);
@@ -166,11 +166,11 @@ __global__ void finish_step(unsigned long long *__restrict__ slots, double max_d
 
 // max(diameter) once per upload (the path never changes diameters)
 template <typename T>
-__global__ void max_diam_kernel(int n, const T *__restrict__ d, unsigned long long *__restrict__ out)
+__global__ void max_diam_kernel(int n, const Rec<T> *__restrict__ rec, unsigned long long *__restrict__ out)
 {
     double v = -INFINITY;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        v = fmax(v, (double)d[i]);
+        v = fmax(v, (double)rec[i].d);
     v = warp_max(v);
     if ((threadIdx.x & 31) == 0 && v != -INFINITY) atomicMax(out, enc_ordered(v));
 }
@@ -211,13 +211,13 @@ __device__ __forceinline__ int flat_box(const Geometry &g, T x, T y, T z)
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads) box_keys(int n, Geometry g, const T *__restrict__ x,
-                                                     const T *__restrict__ y, const T *__restrict__ z,
+__global__ void __launch_bounds__(kThreads) box_keys(int n, Geometry g, const Rec<T> *__restrict__ rec,
                                                      int *__restrict__ count, int2 *__restrict__ key_rank)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int flat = flat_box(g, x[i], y[i], z[i]);
+    const Rec<T> r = rec[i];
+    const int flat = flat_box(g, r.x, r.y, r.z);
     key_rank[i] = make_int2(flat, agg_increment(count, flat));
 }
 
@@ -232,10 +232,10 @@ __global__ void keys_from_flat(int n, const long long *__restrict__ box_index, i
 }
 
 template <typename T>
-__global__ void double_column(int n, T *__restrict__ v)
+__global__ void double_diameter(int n, Rec<T> *__restrict__ rec)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = v[i] * T(2);
+    if (i < n) rec[i].d = rec[i].d * T(2);
 }
 
 // Kernel-level drop-in for kernels.box_ids_parallel: flat ids only (int64).
@@ -438,36 +438,32 @@ __device__ __forceinline__ void put_proxy(const Proxies &P, const Geometry &g, i
 template <typename T, bool RELAYOUT>
 __global__ void __launch_bounds__(kThreads) order_gather(
     int n, Geometry g, BoxDecode bd, const int *__restrict__ tmp, const int2 *__restrict__ key_rank,
-    const int *__restrict__ offset, const T *__restrict__ x, const T *__restrict__ y,
-    const T *__restrict__ z, const T *__restrict__ d, const T *__restrict__ adh,
+    const int *__restrict__ offset, const Rec<T> *__restrict__ rec, const T *__restrict__ adh,
     const uint64_t *__restrict__ uid, int *__restrict__ skey, Proxies prox,
-    int *__restrict__ idx, T *__restrict__ ox_, T *__restrict__ oy_, T *__restrict__ oz_,
-    T *__restrict__ od, T *__restrict__ oadh, uint64_t *__restrict__ ouid, int *__restrict__ pkey)
+    int *__restrict__ idx, Rec<T> *__restrict__ orec, T *__restrict__ oadh, uint64_t *__restrict__ ouid,
+    int *__restrict__ pkey)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     const int i = tmp[s];
     const int k = key_rank[i].x;
     const int o0 = __ldg(offset + k), o1 = __ldg(offset + k + 1);
-    const T zi = z[i];
+    const Rec<T> ri = rec[i];
+    const T zi = ri.z;
     const uint64_t ui = uid[i];
     int q = 0;
     for (int t = o0; t < o1; ++t) {
         const int j = __ldg(tmp + t);
-        const T zj = z[j];
+        const T zj = rec[j].z;
         q += (zj < zi) || (zj == zi && uid[j] < ui);
     }
     const int dst = o0 + q;
     int ix, iy, iz;
     decode_box(bd, k, ix, iy, iz);
-    const T xi = x[i], yi = y[i], di = d[i];
     skey[dst] = k;
-    put_proxy<T>(prox, g, dst, ix, iy, xi, yi, zi);
+    put_proxy<T>(prox, g, dst, ix, iy, ri.x, ri.y, zi);
     if (RELAYOUT) {
-        ox_[dst] = xi;
-        oy_[dst] = yi;
-        oz_[dst] = zi;
-        od[dst] = di;
+        orec[dst] = ri;
         oadh[dst] = adh[i];
         ouid[dst] = ui;
         if (pkey) pkey[dst] = k;
@@ -485,8 +481,7 @@ __global__ void __launch_bounds__(kThreads) order_gather(
 template <typename T>
 __global__ void __launch_bounds__(kThreads) place_full(int n, Geometry g, BoxDecode bd,
                                                        const int2 *__restrict__ key_rank,
-                                                       const int *__restrict__ offset, const T *__restrict__ x,
-                                                       const T *__restrict__ y, const T *__restrict__ z,
+                                                       const int *__restrict__ offset, const Rec<T> *__restrict__ rec,
                                                        int *__restrict__ idx, int *__restrict__ skey,
                                                        Proxies prox, int *__restrict__ pkey)
 {
@@ -498,7 +493,8 @@ __global__ void __launch_bounds__(kThreads) place_full(int n, Geometry g, BoxDec
     decode_box(bd, kr.x, ix, iy, iz);
     idx[slot] = i;
     skey[slot] = kr.x;
-    put_proxy<T>(prox, g, slot, ix, iy, x[i], y[i], z[i]);
+    const Rec<T> r = rec[i];
+    put_proxy<T>(prox, g, slot, ix, iy, r.x, r.y, r.z);
     if (pkey) pkey[i] = kr.x;
 }
 
@@ -506,19 +502,14 @@ __global__ void __launch_bounds__(kThreads) place_full(int n, Geometry g, BoxDec
 // Z-order data sort).  pkey travels with them.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) relayout_records(
-    int n, const int *__restrict__ idx, const T *__restrict__ x, const T *__restrict__ y,
-    const T *__restrict__ z, const T *__restrict__ d, const T *__restrict__ adh,
-    const uint64_t *__restrict__ uid, const int *__restrict__ pkey, T *__restrict__ ox_,
-    T *__restrict__ oy_, T *__restrict__ oz_, T *__restrict__ od, T *__restrict__ oadh,
-    uint64_t *__restrict__ ouid, int *__restrict__ opkey)
+    int n, const int *__restrict__ idx, const Rec<T> *__restrict__ rec, const T *__restrict__ adh,
+    const uint64_t *__restrict__ uid, const int *__restrict__ pkey, Rec<T> *__restrict__ orec,
+    T *__restrict__ oadh, uint64_t *__restrict__ ouid, int *__restrict__ opkey)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     const int i = idx[s];
-    ox_[s] = x[i];
-    oy_[s] = y[i];
-    oz_[s] = z[i];
-    od[s] = d[i];
+    orec[s] = rec[i];
     oadh[s] = adh[i];
     ouid[s] = uid[i];
     if (pkey) opkey[s] = pkey[i];
@@ -541,6 +532,33 @@ __global__ void invert_perm(int n, const int *__restrict__ order, int *__restric
 {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < n) pres[order[r]] = r;
+}
+
+// SoA host columns <-> device records (upload / download).  unpack writes
+// component c of agent i to out[pres ? pres[i] : i].
+template <typename T>
+__global__ void pack_records(int n, const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ z,
+                             const T *__restrict__ d, Rec<T> *__restrict__ rec)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Rec<T> r;
+    r.x = x[i];
+    r.y = y[i];
+    r.z = z[i];
+    r.d = d[i];
+    rec[i] = r;
+}
+
+template <typename T>
+__global__ void unpack_component(int n, const Rec<T> *__restrict__ rec, int c, const int *__restrict__ pres,
+                                 T *__restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const Rec<T> r = rec[i];
+    const T v = c == 0 ? r.x : (c == 1 ? r.y : (c == 2 ? r.z : r.d));
+    out[pres ? pres[i] : i] = v;
 }
 
 // dst[pres[i]] = src[i] (download / export in the reference's order)

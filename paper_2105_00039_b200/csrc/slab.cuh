@@ -26,7 +26,8 @@ struct SlabRecord {
 
 template <typename T>
 struct SlabCols {
-    T *x, *y, *z, *d, *adh, *dx, *dy, *dz;
+    Rec<T> *rec;
+    T *adh, *dx, *dy, *dz;
     uint64_t *uid;
 };
 
@@ -45,12 +46,12 @@ __device__ __forceinline__ int slab_owner(const SlabBounds &B, int ix)
 }
 
 template <typename T>
-__global__ void slab_dest(int n, Geometry g, SlabBounds B, const T *__restrict__ x,
+__global__ void slab_dest(int n, Geometry g, SlabBounds B, const Rec<T> *__restrict__ rec,
                           unsigned char *__restrict__ dest, unsigned long long *__restrict__ counts)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int ix = axis_box((double)x[i], g.ox, g.L, g.gdimx);
+    const int ix = axis_box((double)rec[i].x, g.ox, g.L, g.gdimx);
     const int r = slab_owner(B, ix);
     dest[i] = (unsigned char)r;
     const unsigned peers = __match_any_sync(__activemask(), r);
@@ -74,10 +75,11 @@ __global__ void slab_lists(int n, int n_keep, int rank, const unsigned char *__r
 template <typename T>
 __device__ __forceinline__ void load_record(const SlabCols<T> &C, int i, SlabRecord<T> &r)
 {
-    r.v[0] = C.x[i];
-    r.v[1] = C.y[i];
-    r.v[2] = C.z[i];
-    r.v[3] = C.d[i];
+    const Rec<T> p = C.rec[i];
+    r.v[0] = p.x;
+    r.v[1] = p.y;
+    r.v[2] = p.z;
+    r.v[3] = p.d;
     r.v[4] = C.adh[i];
     r.v[5] = C.dx[i];
     r.v[6] = C.dy[i];
@@ -88,10 +90,12 @@ __device__ __forceinline__ void load_record(const SlabCols<T> &C, int i, SlabRec
 template <typename T>
 __device__ __forceinline__ void store_record(const SlabCols<T> &C, int i, const SlabRecord<T> &r)
 {
-    C.x[i] = r.v[0];
-    C.y[i] = r.v[1];
-    C.z[i] = r.v[2];
-    C.d[i] = r.v[3];
+    Rec<T> p;
+    p.x = r.v[0];
+    p.y = r.v[1];
+    p.z = r.v[2];
+    p.d = r.v[3];
+    C.rec[i] = p;
     C.adh[i] = r.v[4];
     C.dx[i] = r.v[5];
     C.dy[i] = r.v[6];
@@ -150,12 +154,12 @@ __global__ void slab_unpack(int count, int base, const SlabRecord<T> *__restrict
 
 // owned agents in the boundary planes: ix == lo_plane -> list 0, ix == hi_plane -> list 1
 template <typename T>
-__global__ void slab_halo_list(int n, Geometry g, int lo_plane, int hi_plane, const T *__restrict__ x,
+__global__ void slab_halo_list(int n, Geometry g, int lo_plane, int hi_plane, const Rec<T> *__restrict__ rec,
                                int *__restrict__ lo_list, int *__restrict__ hi_list, unsigned *__restrict__ cnt)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int ix = axis_box((double)x[i], g.ox, g.L, g.gdimx);
+    const int ix = axis_box((double)rec[i].x, g.ox, g.L, g.gdimx);
     if (ix == lo_plane) lo_list[atomicAdd(cnt + 0, 1u)] = i;
     if (ix == hi_plane) hi_list[atomicAdd(cnt + 1, 1u)] = i;
 }

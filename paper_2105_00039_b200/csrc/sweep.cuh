@@ -31,7 +31,8 @@ template <typename T>
 struct SweepArgs {
     int n;
     Geometry g;
-    const T *x, *y, *z, *d, *adh;
+    const Rec<T> *rec;
+    const T *adh;
     const uint64_t *uid;
     const int *idx;        // slot -> storage (unsorted mode)
     const int *slot_key;   // slot -> box rank
@@ -40,7 +41,7 @@ struct SweepArgs {
     const int *flat_of;    // rank -> flat, NULL if identity
     Params<T> p;
     T *disp_x, *disp_y, *disp_z;
-    T *new_x, *new_y, *new_z;   // NULL when frozen
+    Rec<T> *new_rec;            // NULL when frozen
     int *rec_m, *rec_nk;        // per storage index, NULL unless recording
     unsigned long long *block_counters;  // 3 per block
 };
@@ -68,18 +69,20 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs<T> A)
         const int z0 = max(iz - 1, 0), z1 = min(iz + 1, A.g.dimz - 1);
 
         const T half = T(0.5);
-        const T xi = A.x[a], yi = A.y[a], zi = A.z[a];
-        const T ri = A.d[a] * half;
+        const Rec<T> me = A.rec[a];
+        const T xi = me.x, yi = me.y, zi = me.z;
+        const T ri = me.d * half;
         const uint64_t ui = A.uid[a];
         const T zero = A.p.zero;
 
         // pair predicate, kernels.py:198-203 (exact expression order)
         auto collides = [&](int j, T &dx, T &dy, T &dz, T &dist, T &rj) -> bool {
-            dx = xi - A.x[j];
-            dy = yi - A.y[j];
-            dz = zi - A.z[j];
+            const Rec<T> o = A.rec[j];
+            dx = xi - o.x;
+            dy = yi - o.y;
+            dz = zi - o.z;
             dist = tsqrt<T>(dx * dx + dy * dy + dz * dz);
-            rj = A.d[j] * half;
+            rj = o.d * half;
             const T delta = (ri + rj) - dist;
             return delta > zero;
         };
@@ -192,10 +195,13 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs<T> A)
         A.disp_x[a] = ddx;
         A.disp_y[a] = ddy;
         A.disp_z[a] = ddz;
-        if (A.new_x) {               // engine.py:325-327 (two-phase: separate buffer)
-            A.new_x[a] = xi + ddx;
-            A.new_y[a] = yi + ddy;
-            A.new_z[a] = zi + ddz;
+        if (A.new_rec) {             // engine.py:325-327 (two-phase: separate buffer)
+            Rec<T> nr;
+            nr.x = xi + ddx;
+            nr.y = yi + ddy;
+            nr.z = zi + ddz;
+            nr.d = me.d;
+            A.new_rec[a] = nr;
         }
         if (A.rec_m) {
             A.rec_m[a] = m;

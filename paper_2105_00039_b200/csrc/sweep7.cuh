@@ -44,13 +44,14 @@ struct Sweep7Args {
     const int *skey;         // slot -> flat box
     const int *idx;          // slot -> storage index, nullptr = identity (relaid out)
     const int *off;          // flat box -> first slot (nb + 1 entries)
-    const T *x, *y, *z, *d, *adh;
+    const Rec<T> *rec;       // x, y, z, diameter (storage order)
+    const T *adh;
     const uint64_t *uid;
     Params<T> p;
     float rmax;              // largest radius of the pool (rounded up)
     float margin;            // absolute prefilter margin
     T *disp_x, *disp_y, *disp_z;
-    T *new_x, *new_y, *new_z;   // nullptr when frozen
+    Rec<T> *new_rec;            // nullptr when frozen
     int *rec_m, *rec_nk;        // storage order, nullptr unless recording
     unsigned long long *slots;  // per-step reduction slots
     double shell_lo[3], shell_hi[3];   // bbox shell: old lo + max move, old hi - max move
@@ -115,7 +116,8 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         const float mey = __ldg(A.prox.xy + 4 * (s >> 1) + 2 + (s & 1));
         const float mez = __ldg(A.prox.z + s);
         const float Lf = (float)A.g.L;
-        const float reach = (float)(A.d[a] * half) + A.rmax + A.margin;
+        const Rec<T> me = A.rec[a];
+        const float reach = (float)(me.d * half) + A.rmax + A.margin;
         const float reach2 = reach * reach;
         const float zhi = mez + reach;
         const f32x2 mz2 = f2_splat(mez);
@@ -174,8 +176,8 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             return mm;
         };
 
-        const T xi = A.x[a], yi = A.y[a], zi = A.z[a];
-        const T ri = A.d[a] * half;
+        const T xi = me.x, yi = me.y, zi = me.z;
+        const T ri = me.d * half;
         T fx = zero, fy = zero, fz = zero;
         int nk = 0, nd = 0;
         T last_rj = T(-1), last_req = zero;
@@ -186,22 +188,19 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             if (p < cnt_ && LST(p) == s) ++p;
             if (p >= cnt_) return;
             int j = A.idx ? __ldg(A.idx + LST(p)) : LST(p);
-            T xj = A.x[j], yj = A.y[j], zj = A.z[j], dj = A.d[j];
+            Rec<T> o = A.rec[j];
 #pragma unroll 1
             while (p < cnt_) {
                 const int jc = j;
-                const T cxj = xj, cyj = yj, czj = zj, cdj = dj;
+                const Rec<T> co = o;
                 ++p;
                 if (p < cnt_ && LST(p) == s) ++p;   // the agent itself
                 if (p < cnt_) {
                     j = A.idx ? __ldg(A.idx + LST(p)) : LST(p);
-                    xj = A.x[j];
-                    yj = A.y[j];
-                    zj = A.z[j];
-                    dj = A.d[j];
+                    o = A.rec[j];
                 }
-                const T dx = xi - cxj, dy = yi - cyj, dz = zi - czj;   // kernels.py:198-203
-                const T rj = cdj * half;
+                const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;   // kernels.py:198-203
+                const T rj = co.d * half;
                 const T dist = tsqrt<T>(dx * dx + dy * dy + dz * dz);
                 const T rsum = ri + rj;
                 const T delta = rsum - dist;
@@ -343,11 +342,14 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         A.disp_x[a] = ddx;
         A.disp_y[a] = ddy;
         A.disp_z[a] = ddz;
-        if (A.new_x) {                 // engine.py:325-327 (separate buffer: two-phase)
+        if (A.new_rec) {               // engine.py:325-327 (separate buffer: two-phase)
             const T nxp = xi + ddx, nyp = yi + ddy, nzp = zi + ddz;
-            A.new_x[a] = nxp;
-            A.new_y[a] = nyp;
-            A.new_z[a] = nzp;
+            Rec<T> nr;
+            nr.x = nxp;
+            nr.y = nyp;
+            nr.z = nzp;
+            nr.d = me.d;
+            A.new_rec[a] = nr;
             // next step's bbox: only agents inside the boundary shell can be extreme
             // (the extreme agent moved by at most max_displacement)
             const double p3[3] = {(double)nxp, (double)nyp, (double)nzp};

@@ -31,7 +31,7 @@ def _ctx(dtype, summation="uid", sweep="v7", relayout_every=1, path="auto"):
     N = _native()
     ctx = N.Context(0, dtype)
     ctx.set_option(N.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[summation])
-    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "v7": 1, "tile": 2}[sweep])
+    ctx.set_option(N.CG_OPT_SWEEP, {"agent": 0, "v7": 1}[sweep])
     ctx.set_option(N.CG_OPT_RELAYOUT_EVERY, relayout_every)
     ctx.set_option(N.CG_OPT_PATH, {"auto": 0, "sparse": 1, "dense": 2}[path])
     return ctx
@@ -71,7 +71,7 @@ def _reference_state(g, k):
 
 @pytest.mark.parametrize("sweep,relayout,path", [
     ("v7", 1, "auto"), ("v7", 1, "sparse"), ("v7", 1, "dense"), ("v7", 2, "sparse"),
-    ("v7", 3, "dense"), ("v7", 1000, "sparse"), ("tile", 1, "sparse"), ("agent", 1, "auto")])
+    ("v7", 3, "dense"), ("v7", 1000, "sparse"), ("agent", 1, "auto")])
 @pytest.mark.parametrize("summation", ["uid", "stencil"])
 @pytest.mark.parametrize("name", golden_names())
 def test_golden(cuda_required, name, summation, sweep, relayout, path):
@@ -85,7 +85,7 @@ def test_golden(cuda_required, name, summation, sweep, relayout, path):
     N = _native()
     ctx = _ctx(dt, summation, sweep=sweep, relayout_every=relayout, path=path)
     # the sparse path always sums in uid order (bit-exact)
-    exact = summation == "uid" or (sweep in ("v7", "tile") and path == "sparse")
+    exact = summation == "uid" or (sweep == "v7" and path == "sparse")
     every = int(g["sort_every"])
     for k in range(int(g["steps"])):
         s = "s%d_" % k

@@ -5,7 +5,7 @@ TAG=${1:-r1}; CFG=${2:-c4}; SUM=${3:-1}; ORD=${4:-1}
 mkdir -p gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_${TAG}_${CFG}.csv python tools/one_step.py $CFG $SUM $ORD 3 > gpurun_out/launches_${TAG}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep7_kernel|sweep_tile" -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep7_kernel|sweep_tile|sweep_pair|sweep7_tiled|sweep_walk|sweep_eval" -c 2 -s 2 \
   -o gpurun_out/prof_${TAG}_${CFG}_sweep python tools/one_step.py $CFG $SUM $ORD 3 > gpurun_out/prof_${TAG}.log 2>&1
 if [ -n "$GRID" ]; then
 timeout 900 ncu --set full --clock-control none -k regex:"box_keys|order_gather|scan_look|place|bbox|finish" -s 7 -c 7 \
