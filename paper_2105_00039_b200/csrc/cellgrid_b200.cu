@@ -60,8 +60,8 @@ struct Buffers {
     void *pscratch = nullptr;        // lazy presentation sort scratch
     size_t pscratch_bytes = 0;
     int *rec_m = nullptr, *rec_nk = nullptr;
-    float *prox = nullptr;           // Proxies: xy (4 floats per slot pair) then z
-    Proxies P() const { return Proxies{prox, prox + 4 * pairs}; }
+    float *prox = nullptr;           // Proxies: 8 floats per slot pair
+    Proxies P() const { return Proxies{prox}; }
     int64_t pairs = 0;
     void *stage = nullptr;           // download staging (n x 8 B)
 };
@@ -178,8 +178,8 @@ static int alloc_agents(cg_context *c, int64_t cap)
     int **ints[] = {&b.tmp, &b.idx, &b.skey, &b.pres, &b.rec_m, &b.rec_nk, &b.pkey[0], &b.pkey[1], &b.ovf};
     for (int **p : ints) CUDA_TRY(c, cudaMalloc(p, ie));
     b.pairs = cap / 2 + 8;   // the sweep may read a few pairs past n
-    CUDA_TRY(c, cudaMalloc(&b.prox, sizeof(float) * 6 * (size_t)b.pairs));
-    CUDA_TRY(c, cudaMemset(b.prox, 0, sizeof(float) * 6 * (size_t)b.pairs));
+    CUDA_TRY(c, cudaMalloc(&b.prox, sizeof(float) * 8 * (size_t)b.pairs));
+    CUDA_TRY(c, cudaMemset(b.prox, 0, sizeof(float) * 8 * (size_t)b.pairs));
     CUDA_TRY(c, cudaMalloc(&b.stage, 8 * (size_t)cap));
     c->cap = cap;
     return CG_OK;

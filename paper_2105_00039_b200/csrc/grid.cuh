@@ -409,25 +409,24 @@ __global__ void __launch_bounds__(kThreads) place(int n, const int2 *__restrict_
     tmp[__ldg(offset + kr.x) + kr.y] = i;
 }
 
-// fp32 proxies in slot order, pair-interleaved so the sweep tests two
-// candidates per packed FADD2/FFMA2 chain:
-//   xy[4q .. 4q+3] = (x_2q, x_2q+1, y_2q, y_2q+1)   box-local x/y (|err| <= ulp(L))
-//   z[2q .. 2q+1]  = (z_2q, z_2q+1)                  grid-relative z (monotone, so
-//                                                    z-sorted boxes stay sorted)
-// The candidate's radius is not stored: the sweep bounds it by the pool's
-// largest radius (conservative).
+// fp32 proxies in slot order, one 32-byte record per slot pair so the sweep
+// loads two candidates with one sector pair and tests them with one packed
+// FADD2/FFMA2 chain:
+//   p[8q .. 8q+7] = (x_2q, x_2q+1, y_2q, y_2q+1, z_2q, z_2q+1, -, -)
+// x/y box-local (|err| <= ulp(L)), z grid-relative (monotone, so z-sorted
+// boxes stay sorted).  The candidate's radius is not stored: the sweep bounds
+// it by the pool's largest radius (conservative).
 struct Proxies {
-    float *xy;
-    float *z;
+    float *p;
 };
 
 template <typename T>
 __device__ __forceinline__ void put_proxy(const Proxies &P, const Geometry &g, int s, int ix, int iy, T x, T y, T z)
 {
-    const int q = s >> 1, h = s & 1;
-    P.xy[4 * q + h] = (float)((double)x - (g.ox + (double)(ix + g.xoff) * g.L));
-    P.xy[4 * q + 2 + h] = (float)((double)y - (g.oy + (double)iy * g.L));
-    P.z[s] = (float)((double)z - g.oz);
+    float *r = P.p + 8 * (s >> 1) + (s & 1);
+    r[0] = (float)((double)x - (g.ox + (double)(ix + g.xoff) * g.L));
+    r[2] = (float)((double)y - (g.oy + (double)iy * g.L));
+    r[4] = (float)((double)z - g.oz);
 }
 
 // Members of a box are re-ranked by (z, uid) -- a pure function of the

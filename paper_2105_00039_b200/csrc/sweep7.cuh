@@ -112,9 +112,8 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         const int a = A.idx ? __ldg(A.idx + s) : s;
         if (a >= A.n_owned) return;   // a ghost: candidate only
         const T half = T(0.5), zero = A.p.zero;
-        const float mex = __ldg(A.prox.xy + 4 * (s >> 1) + (s & 1));
-        const float mey = __ldg(A.prox.xy + 4 * (s >> 1) + 2 + (s & 1));
-        const float mez = __ldg(A.prox.z + s);
+        const float *myp = A.prox.p + 8 * (s >> 1) + (s & 1);
+        const float mex = __ldg(myp), mey = __ldg(myp + 2), mez = __ldg(myp + 4);
         const float Lf = (float)A.g.L;
         const Rec<T> me = A.rec[a];
         const float reach = (float)(me.d * half) + A.rmax + A.margin;
@@ -122,8 +121,8 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         const float zhi = mez + reach;
         const f32x2 mz2 = f2_splat(mez);
         const int z0 = max(iz - 1, 0), z1 = min(iz + 1, A.g.dimz - 1);
-        const ulonglong2 *PXY = reinterpret_cast<const ulonglong2 *>(A.prox.xy);
-        const f32x2 *PZ = reinterpret_cast<const f32x2 *>(A.prox.z);
+        // slot pair q = ta / 2 lives in 16-byte words 2q (x pair, y pair) and 2q + 1 (z pair)
+        const ulonglong2 *PR = reinterpret_cast<const ulonglong2 *>(A.prox.p);
 
         // phase-1 walk over the 9 stencil columns; visit(t) per survivor, in
         // slot order (the agent itself included: phase 2 skips it); after()
@@ -146,29 +145,42 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                     const float gy = oy == 0 ? 0.f : fmaxf(0.f, oy < 0 ? mey : Lf - mey);
                     if (gx * gx + gy * gy > reach2) continue;
                     const f32x2 my2 = f2_splat(mey - (float)oy * Lf);
-                    // slot pairs covering [t0, t1); the proxy arrays are padded past n
-                    for (int ta = t0 & ~1; ta < t1; ta += 2) {
-                        const ulonglong2 xy = __ldg(PXY + (ta >> 1));
-                        const f32x2 zz = __ldg(PZ + (ta >> 1));
-                        const f32x2 dz = f2_sub(mz2, zz);
-                        f32x2 d2 = f2_mul(dz, dz);
-                        const f32x2 dy = f2_sub(my2, xy.y);
-                        d2 = f2_fma(dy, dy, d2);
-                        const f32x2 dx = f2_sub(mx2, xy.x);
-                        d2 = f2_fma(dx, dx, d2);
-                        float d2a, d2b;
-                        f2_unpack(d2, d2a, d2b);
-                        const bool pa = d2a <= reach2 && ta >= t0;
-                        const bool pb = d2b <= reach2 && ta + 1 < t1;
-                        if (pa || pb) {
-                            if (pa) visit(ta);
-                            if (pb) visit(ta + 1);
+                    // two slot pairs per iteration (both loads in flight); the proxy
+                    // array is padded past n, masks drop slots outside [t0, t1)
+                    for (int ta = t0 & ~1; ta < t1; ta += 4) {
+                        const ulonglong2 xa = __ldg(PR + ta), za = __ldg(PR + ta + 1);
+                        const ulonglong2 xb = __ldg(PR + ta + 2), zb = __ldg(PR + ta + 3);
+                        f32x2 d, ea, eb;
+                        d = f2_sub(mz2, za.x);
+                        ea = f2_mul(d, d);
+                        d = f2_sub(mz2, zb.x);
+                        eb = f2_mul(d, d);
+                        d = f2_sub(my2, xa.y);
+                        ea = f2_fma(d, d, ea);
+                        d = f2_sub(my2, xb.y);
+                        eb = f2_fma(d, d, eb);
+                        d = f2_sub(mx2, xa.x);
+                        ea = f2_fma(d, d, ea);
+                        d = f2_sub(mx2, xb.x);
+                        eb = f2_fma(d, d, eb);
+                        float a0, a1, b0, b1;
+                        f2_unpack(ea, a0, a1);
+                        f2_unpack(eb, b0, b1);
+                        const bool p0 = a0 <= reach2 && ta >= t0;
+                        const bool p1 = a1 <= reach2 && ta + 1 < t1;
+                        const bool p2 = b0 <= reach2 && ta + 2 < t1;
+                        const bool p3 = b1 <= reach2 && ta + 3 < t1;
+                        if (p0 | p1 | p2 | p3) {
+                            if (p0) visit(ta);
+                            if (p1) visit(ta + 1);
+                            if (p2) visit(ta + 2);
+                            if (p3) visit(ta + 3);
                             after();
                         }
                         if (ZSORTED) {
-                            float za, zb;
-                            f2_unpack(zz, za, zb);
-                            if (zb > zhi) break;   // z-sorted run (zb past t1 only ends the loop sooner)
+                            float zl, zh;
+                            f2_unpack(zb.x, zl, zh);
+                            if (zh > zhi) break;   // z-sorted run (past t1 only ends the loop sooner)
                         }
                     }
                 }
@@ -235,7 +247,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             int ns = 0;
             m = walk([&](int t) { LST(ns++) = t; },
                      [&]() {
-                         if (ns > KS - 2) {
+                         if (ns > KS - 4) {   // a batch appends up to 4
                              evaluate(ns);
                              ns = 0;
                          }
