@@ -31,6 +31,10 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "../../include/cellgrid_b200.h"
+
+#ifndef CG_SPARSE_MINB
+#define CG_SPARSE_MINB 4   // resident 256-thread CTAs per SM for the sparse sweep (measured)
+#endif
 #include "common.cuh"
 #include "grid.cuh"
 #include "sweep.cuh"
@@ -406,17 +410,22 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
     const int a = c->cur_attr, o = 1 - c->cur_pos, oa = 1 - c->cur_attr;
     int *pk = sort ? c->b.pkey[a] : nullptr;
     if (!dense) {
-        place_full<T><<<nblk, kThreads, 0, st>>>(n, g, c->bd, c->b.key_rank, c->offset, rec, c->b.idx,
-                                                 c->b.skey, c->b.P(), pk);
-        LAUNCH_CHECK(c);
-        c->launches += 1;
-        CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
         if (relayout) {
-            relayout_records<T><<<nblk, kThreads, 0, st>>>(
-                n, c->b.idx, rec, (T *)c->b.adh[a], c->b.uid[a], pk, (Rec<T> *)c->b.rec[o],
-                (T *)c->b.adh[oa], c->b.uid[oa], c->b.pkey[oa]);
+            // records move straight to their slots (storage becomes slot order);
+            // pkey carries the last sort step's box (this step's on a sort step)
+            place_relayout<T><<<nblk, kThreads, 0, st>>>(
+                n, g, c->bd, c->b.key_rank, c->offset, rec, (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(),
+                sort ? nullptr : c->b.pkey[a], c->b.pkey[oa], (Rec<T> *)c->b.rec[o], (T *)c->b.adh[oa],
+                c->b.uid[oa]);
             LAUNCH_CHECK(c);
             c->launches += 1;
+            CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
+        } else {
+            place_full<T><<<nblk, kThreads, 0, st>>>(n, g, c->bd, c->b.key_rank, c->offset, rec, c->b.idx,
+                                                     c->b.skey, c->b.P(), pk);
+            LAUNCH_CHECK(c);
+            c->launches += 1;
+            CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
         }
     } else {
         place<<<nblk, kThreads, 0, st>>>(n, c->b.key_rank, c->offset, c->b.tmp);
@@ -472,7 +481,7 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         // sparse: survivors summed in uid order (deterministic and bit-identical to
         // the reference whatever the slot order in a box); agents with more than
         // 16 survivors go to the overflow kernel
-        return launch_sweep7_k<T, true, false, 16, false, 4>(c, A);
+        return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB>(c, A);
     }
     if (c->summation == SUM_UID) return launch_sweep7_k<T, true, true, 16, false, 3>(c, A);
     // dense, stencil order: the list is evaluated whenever it fills

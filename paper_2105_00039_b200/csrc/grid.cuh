@@ -497,6 +497,31 @@ __global__ void __launch_bounds__(kThreads) place_full(int n, Geometry g, BoxDec
     if (pkey) pkey[i] = kr.x;
 }
 
+// place_full + relayout in one pass: the agent's whole record goes straight
+// to its slot (storage becomes slot order; no slot -> storage index needed).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) place_relayout(
+    int n, Geometry g, BoxDecode bd, const int2 *__restrict__ key_rank, const int *__restrict__ offset,
+    const Rec<T> *__restrict__ rec, const T *__restrict__ adh, const uint64_t *__restrict__ uid,
+    int *__restrict__ skey, Proxies prox, const int *__restrict__ pkey_sort_in, int *__restrict__ pkey_out,
+    Rec<T> *__restrict__ orec, T *__restrict__ oadh, uint64_t *__restrict__ ouid)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int2 kr = key_rank[i];
+    const int slot = __ldg(offset + kr.x) + kr.y;
+    int ix, iy, iz;
+    decode_box(bd, kr.x, ix, iy, iz);
+    const Rec<T> r = rec[i];
+    skey[slot] = kr.x;
+    put_proxy<T>(prox, g, slot, ix, iy, r.x, r.y, r.z);
+    orec[slot] = r;
+    oadh[slot] = adh[i];
+    ouid[slot] = uid[i];
+    // pkey: this step's box when it is a sort step, else the carried value
+    if (pkey_out) pkey_out[slot] = pkey_sort_in ? pkey_sort_in[i] : kr.x;
+}
+
 // Move the records into slot order (locality for the sweep; the paper's
 // Z-order data sort).  pkey travels with them.
 template <typename T>
