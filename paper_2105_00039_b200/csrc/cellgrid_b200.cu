@@ -289,6 +289,20 @@ static int launch_scan(cg_context *c, bool morton, int nb, int *out, unsigned lo
     return CG_OK;
 }
 
+// Reduce-then-scan of the per-box counts into offsets (zeroes the counts).
+static int launch_scan_rts(cg_context *c, int nb, unsigned long long *stat)
+{
+    const int ntiles = cdiv(nb, kScanTile);
+    cudaStream_t st = c->stream;
+    int *tile_sum = reinterpret_cast<int *>(c->scan_status);   // >= ntiles ints
+    scan_reduce<<<ntiles, kThreads, 0, st>>>(nb, c->count, tile_sum);
+    scan_tilesums<<<1, 1024, 0, st>>>(ntiles, tile_sum);
+    scan_down<<<ntiles, kThreads, 0, st>>>(nb, c->count, tile_sum, c->offset, stat);
+    LAUNCH_CHECK(c);
+    c->launches += 3;
+    return CG_OK;
+}
+
 // Standalone bbox of the stored positions into bbox_host (synchronous).
 template <typename T>
 static int standalone_bbox(cg_context *c)
@@ -399,10 +413,10 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
     CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
     const int nblk = cdiv(n, kThreads);
     const Rec<T> *rec = (const Rec<T> *)c->b.rec[c->cur_pos];
-    box_keys<T><<<nblk, kThreads, 0, st>>>(n, g, rec, c->count, c->b.key_rank);
+    box_keys<T><<<nblk, kThreads, 0, st>>>(n, g, 1.0 / g.L, rec, c->count, c->b.key_rank);
     LAUNCH_CHECK(c);
     c->launches += 1;
-    if ((rc = launch_scan(c, false, g.nb, c->offset, stat))) return rc;
+    if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
     // sparse pools (few agents per box): the scatter is the CSR; dense pools
     // also order each box by (z, uid) so column runs can be cut on z
     const double surv = 4.19 * (double)n / (double)g.nb;   // expected survivors per agent

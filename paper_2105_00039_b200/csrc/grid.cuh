@@ -201,6 +201,32 @@ __device__ __forceinline__ int axis_box(double p, double o, double L, int dim)
     return (int)k;
 }
 
+// Same value as axis_box without the IEEE division: t = (p - o) * (1/L) is
+// within a few ulp of the correctly rounded quotient, so floor(t) is exact
+// unless t lies within that distance of an integer -- only then divide.
+__device__ __forceinline__ int axis_box_fast(double p, double o, double L, double invL, int dim)
+{
+    const double q = p - o;
+    const double t = q * invL;
+    const double k = floor(t);
+    double f;
+    if (t - k > 1e-12 * fabs(t) + 1e-300 && (k + 1.0) - t > 1e-12 * fabs(t) + 1e-300) f = k;
+    else f = floor(q / L);   // near a box face: the reference's expression
+    long long kk = (long long)f;
+    if (kk < 0) kk = 0;
+    else if (kk >= dim) kk = dim - 1;
+    return (int)kk;
+}
+
+template <typename T>
+__device__ __forceinline__ int flat_box_fast(const Geometry &g, double invL, T x, T y, T z)
+{
+    const int ix = axis_box_fast((double)x, g.ox, g.L, invL, g.gdimx) - g.xoff;
+    const int iy = axis_box_fast((double)y, g.oy, g.L, invL, g.dimy);
+    const int iz = axis_box_fast((double)z, g.oz, g.L, invL, g.dimz);
+    return (ix * g.dimy + iy) * g.dimz + iz;
+}
+
 template <typename T>
 __device__ __forceinline__ int flat_box(const Geometry &g, T x, T y, T z)
 {
@@ -210,15 +236,31 @@ __device__ __forceinline__ int flat_box(const Geometry &g, T x, T y, T z)
     return (ix * g.dimy + iy) * g.dimz + iz;
 }
 
+// Ranks within a box come from one atomicAdd per run of equal keys in the
+// warp (storage is box-sorted from the previous step, so keys arrive in runs;
+// a key split over several runs just takes several atomics).
 template <typename T>
-__global__ void __launch_bounds__(kThreads) box_keys(int n, Geometry g, const Rec<T> *__restrict__ rec,
+__global__ void __launch_bounds__(kThreads) box_keys(int n, Geometry g, double invL, const Rec<T> *__restrict__ rec,
                                                      int *__restrict__ count, int2 *__restrict__ key_rank)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const Rec<T> r = rec[i];
-    const int flat = flat_box(g, r.x, r.y, r.z);
-    key_rank[i] = make_int2(flat, agg_increment(count, flat));
+    const int lane = threadIdx.x & 31;
+    int flat = -1 - lane;   // distinct dummy keys for lanes past n
+    if (i < n) {
+        const Rec<T> r = rec[i];
+        flat = flat_box_fast(g, invL, r.x, r.y, r.z);
+    }
+    const int prev = __shfl_up_sync(0xffffffffu, flat, 1);
+    const bool start = lane == 0 || prev != flat;
+    const unsigned starts = __ballot_sync(0xffffffffu, start);
+    const unsigned upto = starts & (0xffffffffu >> (31 - lane));   // run starts at or below lane
+    const int leader = 31 - __clz(upto);
+    const unsigned after = starts & ~(0xffffffffu >> (31 - leader));   // starts above the leader
+    const int run_end = after ? __ffs(after) - 1 : 32;
+    int base = 0;
+    if (start && i < n) base = atomicAdd(count + flat, run_end - lane);
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (i < n) key_rank[i] = make_int2(flat, base + (lane - leader));
 }
 
 // Keys from caller-supplied flat box ids (kernel-level force-phase drop-in).
@@ -293,6 +335,129 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int &total)
     total = block_tot;
     __syncthreads();  // warp_off / block_tot are reused by the next call
     return excl;
+}
+
+// Reduce-then-scan (grid path): scan_reduce writes each tile's sum,
+// scan_tilesums scans them in one CTA, scan_down produces the offsets,
+// zeroes the counts and accumulates the grid statistics.
+__device__ __forceinline__ void load_tile(int nb, const int *__restrict__ count, int base, int v[kScanItems])
+{
+    if (base + kScanItems <= nb) {
+        const int4 *p = reinterpret_cast<const int4 *>(count + base);
+#pragma unroll
+        for (int q = 0; q < kScanItems / 4; ++q) {
+            const int4 u = p[q];
+            v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) v[k] = base + k < nb ? count[base + k] : 0;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) scan_reduce(int nb, const int *__restrict__ count,
+                                                        int *__restrict__ tile_sum)
+{
+    int v[kScanItems];
+    load_tile(nb, count, blockIdx.x * kScanTile + threadIdx.x * kScanItems, v);
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) s += v[k];
+    s = __reduce_add_sync(0xffffffffu, (unsigned)s);
+    __shared__ int ws[kThreads / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < kThreads / 32; ++w) t += ws[w];
+        tile_sum[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) scan_tilesums(int ntiles, int *__restrict__ tile_sum)
+{
+    // exclusive scan in place, 1024 threads, any count
+    __shared__ int warp_tot[32];
+    __shared__ int carry_sh;
+    if (threadIdx.x == 0) carry_sh = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < ntiles; base += 1024) {
+        const int i = base + threadIdx.x;
+        const int v = i < ntiles ? tile_sum[i] : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) warp_tot[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const int t = warp_tot[lane];
+            int s2 = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, s2, o);
+                if (lane >= o) s2 += u;
+            }
+            warp_tot[lane] = s2 - t;
+        }
+        __syncthreads();
+        const int carry = carry_sh;
+        if (i < ntiles) tile_sum[i] = carry + warp_tot[w] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_sh = carry + warp_tot[31] + inc;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) scan_down(int nb, int *__restrict__ count,
+                                                      const int *__restrict__ tile_sum, int *__restrict__ offset,
+                                                      unsigned long long *__restrict__ stat)
+{
+    const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+    int v[kScanItems];
+    load_tile(nb, count, base, v);
+    int s = 0, occ = 0, mx = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        s += v[k];
+        occ += v[k] > 0;
+        mx = max(mx, v[k]);
+    }
+    int total;
+    int run = block_exclusive_scan(s, total) + tile_sum[blockIdx.x];
+    if (base + kScanItems <= nb) {
+        int4 *po = reinterpret_cast<int4 *>(offset + base);
+        int4 *pc = reinterpret_cast<int4 *>(count + base);
+#pragma unroll
+        for (int q = 0; q < kScanItems / 4; ++q) {
+            int4 o;
+            o.x = run; run += v[4 * q];
+            o.y = run; run += v[4 * q + 1];
+            o.z = run; run += v[4 * q + 2];
+            o.w = run; run += v[4 * q + 3];
+            po[q] = o;
+            pc[q] = make_int4(0, 0, 0, 0);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            if (base + k < nb) {
+                offset[base + k] = run;
+                count[base + k] = 0;
+            }
+            run += v[k];
+        }
+    }
+    if (base <= nb - 1 && nb - 1 < base + kScanItems) offset[nb] = run;
+    occ = __reduce_add_sync(0xffffffffu, (unsigned)occ);
+    mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)mx);
+    if ((threadIdx.x & 31) == 0 && stat) {
+        if (occ) atomicAdd(stat + 0, (unsigned long long)occ);
+        if (mx) atomicMax(stat + 1, (unsigned long long)mx);
+    }
 }
 
 template <bool MORTON>

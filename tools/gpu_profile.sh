@@ -8,7 +8,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep7_kernel|sweep_tile|sweep_pair|sweep7_tiled|sweep_walk|sweep_eval" -c 2 -s 2 \
   -o gpurun_out/prof_${TAG}_${CFG}_sweep python tools/one_step.py $CFG $SUM $ORD 3 > gpurun_out/prof_${TAG}.log 2>&1
 if [ -n "$GRID" ]; then
-timeout 900 ncu --set full --clock-control none -k regex:"box_keys|scan_look|place" -s 6 -c 3 \
+timeout 900 ncu --set full --clock-control none -k regex:"box_keys|scan_look|place" -s 3 -c 3 \
   -o gpurun_out/prof_${TAG}_${CFG}_grid python tools/one_step.py $CFG $SUM $ORD 2 >> gpurun_out/prof_${TAG}.log 2>&1
 fi
 ls -la gpurun_out
