@@ -40,6 +40,7 @@
 #include "sweep.cuh"
 #include "sweep7.cuh"
 #include "slab.cuh"
+#include "sweep_warp.cuh"
 
 using namespace cg;
 
@@ -497,9 +498,35 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         // 16 survivors go to the overflow kernel
         return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB>(c, A);
     }
-    if (c->summation == SUM_UID) return launch_sweep7_k<T, true, true, 16, false, 3>(c, A);
-    // dense, stencil order: the list is evaluated whenever it fills
-    return launch_sweep7_k<T, false, true, 32, true, 3>(c, A);
+    // moderately dense (<= 20 expected survivors): one thread per agent
+    const double surv = 4.19 * (double)A.n / (double)c->geo.nb;
+    if (surv <= 20.0) {
+        if (c->summation == SUM_UID) return launch_sweep7_k<T, true, true, 16, false, 3>(c, A);
+        return launch_sweep7_k<T, false, true, 32, true, 3>(c, A);   // list evaluated whenever it fills
+    }
+    // dense: one warp per agent (warp-cooperative walk, survivors compacted
+    // into a per-warp queue); uid order bit-exact, stencil order deterministic
+    cudaStream_t st = c->stream;
+    const int blocks = std::min(cdiv(A.n, kThreads / 32), 148 * 16);
+    CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
+    if (c->summation == SUM_UID) {
+        auto k = sweep_warp_kernel<T, true>;
+        const size_t sm = sizeof(WarpSmem<T, true>);
+        CUDA_TRY(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k<<<blocks, kThreads, sm, st>>>(A);
+        LAUNCH_CHECK(c);
+        sweep7_overflow<T, true, true, 16><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
+        LAUNCH_CHECK(c);
+        c->launches += 2;
+    } else {
+        auto k = sweep_warp_kernel<T, false>;
+        const size_t sm = sizeof(WarpSmem<T, false>);
+        CUDA_TRY(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k<<<blocks, kThreads, sm, st>>>(A);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+    }
+    return CG_OK;
 }
 
 template <typename T>
