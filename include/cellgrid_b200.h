@@ -130,6 +130,17 @@ int cg_force_phase(cg_context *ctx, int64_t n, const void *px, const void *py, c
                    const void *params7, void *out_dx, void *out_dy, void *out_dz,
                    int64_t counters[3]);
 
+/* ---- radius queries: kernels.grid_neighbor_counts /
+ * grid_neighbor_fill (kernels.py:427-520) behind spatial.neighbor_counts /
+ * neighbor_csr (spatial.py:158-169).  Closed-ball f64 predicate
+ * d2 <= radius^2 over the 27-box stencil of the grid built by cg_build_grid
+ * (CG_ERR_STATE otherwise); radius <= box_length (CG_ERR_STENCIL).  Agents
+ * and neighbour indices are in the reference's storage order; every row of the
+ * CSR table ascends by neighbour uid.  counts: n int64; indptr: n + 1 int64
+ * (exclusive prefix of the counts); indices: indptr[n] int64. */
+int cg_neighbor_counts(cg_context *ctx, double radius, int64_t *counts);
+int cg_neighbor_fill(cg_context *ctx, double radius, const int64_t *indptr, int64_t *indices);
+
 /* ---- x-slab decomposition (multi-GPU).  The reference has no
  * distributed layer: these entry points carry the same step across ranks,
  * one context per GPU.  Device buffers (send/recv) are raw device pointers

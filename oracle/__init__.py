@@ -7,7 +7,7 @@ reference functions and DESIGN.md ("Oracle") for how it is pinned.
 """
 
 from .oracle import (OracleError, OracleGridOverflow, OracleStep, all_pairs, box_ids,
-                     build, csr, force_phase, geometry, lib, morton_encode, morton_perm, step)
+                     build, csr, force_phase, geometry, lib, morton_encode, morton_perm, neighbor_csr, step)
 
 __all__ = ["OracleError", "OracleGridOverflow", "OracleStep", "all_pairs", "box_ids", "build",
            "csr", "force_phase", "geometry", "lib", "morton_encode", "morton_perm", "step"]

@@ -202,3 +202,36 @@ def step(pool, params, sort=True, freeze=False, interaction_radius=None, threads
                       degenerate_pairs=int(counters[2]), box_length=L, origin=origin,
                       dims=dims, box_index=bidx, box_count=count, box_offsets=start,
                       m=m, nk=nk, perm=perm)
+
+
+def neighbor_csr(px, py, pz, uid, radius, block=1024):
+    """Radius-query table by brute force -- the predicate of reference
+    kernels._grid_count_one / grid_neighbor_fill (kernels.py:427-520): widen to
+    f64, dx = p_j - p_i per axis, d2 = (dx*dx + dy*dy) + dz*dz, keep j != i
+    with d2 <= radius^2 (closed ball); each row ascends by neighbour uid
+    (kernels._sort_row_by_uid, kernels.py:471-480).  The grid only restricts
+    candidates to the 27-box stencil, which holds every agent within
+    radius <= box_length, so the all-pairs table is the same table.
+    Returns (indptr, indices) in storage order (numpy, O(n^2) in blocks)."""
+    x = np.asarray(px).astype(np.float64)
+    y = np.asarray(py).astype(np.float64)
+    z = np.asarray(pz).astype(np.float64)
+    uid = np.asarray(uid)
+    n = x.shape[0]
+    r2 = float(radius) * float(radius)
+    by_uid = np.argsort(uid, kind="stable")
+    rows = []
+    for a in range(0, n, block):
+        b = min(n, a + block)
+        dx = x[by_uid][None, :] - x[a:b, None]
+        dy = y[by_uid][None, :] - y[a:b, None]
+        dz = z[by_uid][None, :] - z[a:b, None]
+        hit = (dx * dx + dy * dy) + dz * dz <= r2
+        hit[np.arange(b - a), np.searchsorted(uid[by_uid], uid[a:b])] = False
+        for r in range(b - a):
+            rows.append(by_uid[hit[r]])
+    counts = np.array([len(r) for r in rows], np.int64)
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=indptr[1:])
+    indices = np.concatenate(rows).astype(np.int64) if n else np.zeros(0, np.int64)
+    return indptr, indices

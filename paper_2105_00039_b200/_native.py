@@ -30,7 +30,7 @@ EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_
             "cg_record_export", "cg_box_ids", "cg_force_phase", "cg_launch_count",
             "cg_host_alloc", "cg_host_free", "cg_record_bytes", "cg_reserve", "cg_local_bbox",
             "cg_slab_plan", "cg_slab_migrate", "cg_slab_accept", "cg_slab_halo",
-            "cg_slab_set_ghosts", "cg_slab_step")
+            "cg_slab_set_ghosts", "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill")
 
 
 class GridOverflowError(RuntimeError):
@@ -96,6 +96,8 @@ def load():
         "cg_box_ids": ([_P, _I64, _P, _P, _P] + [ctypes.c_double] * 4 + [_I64] * 3 + [_P],
                        ctypes.c_int),
         "cg_force_phase": ([_P, _I64] + [_P] * 7 + [_I64] * 3 + [_P] * 5, ctypes.c_int),
+        "cg_neighbor_counts": ([_P, ctypes.c_double, _P], ctypes.c_int),
+        "cg_neighbor_fill": ([_P, ctypes.c_double, _P, _P], ctypes.c_int),
         "cg_record_bytes": ([_P], _I64),
         "cg_reserve": ([_P, _I64], ctypes.c_int),
         "cg_local_bbox": ([_P, _P], ctypes.c_int),
@@ -226,6 +228,20 @@ class Context:
         bc = np.empty(num_boxes, np.int64)
         check(load().cg_grid_export(self.h, ptr(bi), ptr(bc)), self.h)
         return bi, bc
+
+    # ---- radius queries (spatial.neighbor_counts / neighbor_csr)
+    def neighbor_counts(self, radius):
+        out = np.empty(self.n, np.int64)
+        check(load().cg_neighbor_counts(self.h, float(radius), ptr(out)), self.h)
+        return out
+
+    def neighbor_csr(self, radius):
+        counts = self.neighbor_counts(radius)
+        indptr = np.zeros(self.n + 1, np.int64)
+        np.cumsum(counts, out=indptr[1:])
+        indices = np.empty(int(indptr[-1]), np.int64)
+        check(load().cg_neighbor_fill(self.h, float(radius), ptr(indptr), ptr(indices)), self.h)
+        return indptr, indices
 
     # ---- x-slab decomposition (see include/cellgrid_b200.h and distributed.py)
     @property

@@ -41,6 +41,7 @@
 #include "sweep7.cuh"
 #include "slab.cuh"
 #include "sweep_warp.cuh"
+#include "query.cuh"
 
 using namespace cg;
 
@@ -109,6 +110,7 @@ struct cg_context {
     int pres_state = PRES_IDENTITY;
     bool last_record = false;
     bool last_dense = false;
+    bool grid_current = false;    // the grid indexes the stored positions (cg_build_grid)
     int64_t sort_steps = 0;
     Geometry geo_sort{};          // geometry of the last sort step (presentation order)
     // options
@@ -1087,6 +1089,7 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
     }
     c->n = n;
     c->n_owned = n;
+    c->grid_current = false;
     c->slab.planned = false;
     c->cur_pos = c->cur_attr = 0;
     c->have_grid = false;
@@ -1173,6 +1176,7 @@ int cg_step(cg_context *c, const double params[5], double interaction_radius, in
     if (!c) return CG_ERR_VALUE;
     CUDA_TRY(c, cudaSetDevice(c->device));
     int64_t id = -1;
+    c->grid_current = false;
     const int rc = c->prec == CG_FP64
                        ? step_impl<double>(c, params, interaction_radius, box_cap, flags, &id)
                        : step_impl<float>(c, params, interaction_radius, box_cap, flags, &id);
@@ -1193,6 +1197,7 @@ int cg_build_grid(cg_context *c, double interaction_radius, int64_t box_cap, cg_
                        ? build_grid<double>(c, interaction_radius, box_cap, false, false, origin, dims64)
                        : build_grid<float>(c, interaction_radius, box_cap, false, false, origin, dims64);
     if (rc) return rc;
+    c->grid_current = true;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (stats) {
         std::memset(stats, 0, sizeof *stats);
@@ -1465,5 +1470,94 @@ int cg_slab_step(cg_context *c, const double params[5], int flags, cg_step_stats
     return CG_OK;
 }
 
+// ---------------------------------------------------------------- radius queries
 }  // extern "C"
+
+template <typename T>
+static int neighbor_query_t(cg_context *c, double radius, int64_t *counts, const int64_t *indptr,
+                            int64_t *indices)
+{
+    const int n = (int)c->n;
+    cudaStream_t st = c->stream;
+    int rc = materialize_presentation(c);
+    if (rc) return rc;
+    QueryArgs<T> Q{};
+    Q.n = n;
+    Q.g = c->geo;
+    Q.bd = c->bd;
+    Q.skey = c->b.skey;
+    Q.idx = c->relaid ? nullptr : c->b.idx;
+    Q.off = c->offset;
+    Q.rec = (const Rec<T> *)c->b.rec[c->cur_pos];
+    Q.uid = c->b.uid[c->cur_attr];
+    Q.pres = c->pres_state == PRES_IDENTITY ? nullptr : c->b.pres;
+    Q.r2 = radius * radius;
+    if (counts) {
+        Q.counts = (long long *)c->b.stage;
+        neighbor_kernel<T, false><<<cdiv(n, kThreads), kThreads, 0, st>>>(Q);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        CUDA_TRY(c, cudaMemcpyAsync(counts, c->b.stage, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        return CG_OK;
+    }
+    const int64_t total = indptr[n];
+    long long *dptr = nullptr, *dind = nullptr;
+    int *inv = nullptr;
+    CUDA_TRY(c, cudaMallocAsync(&dptr, sizeof(long long) * (n + 1), st));
+    CUDA_TRY(c, cudaMallocAsync(&dind, sizeof(long long) * std::max<int64_t>(total, 1), st));
+    CUDA_TRY(c, cudaMemcpyAsync(dptr, indptr, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, st));
+    Q.indptr = dptr;
+    Q.indices = dind;
+    neighbor_kernel<T, true><<<cdiv(n, kThreads), kThreads, 0, st>>>(Q);
+    if (Q.pres) {   // reference position -> storage index, for the uids of row entries
+        CUDA_TRY(c, cudaMallocAsync(&inv, sizeof(int) * n, st));
+        invert_perm<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, Q.pres, inv);
+    }
+    sort_rows_by_uid<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, dptr, dind, inv, Q.uid);
+    LAUNCH_CHECK(c);
+    c->launches += Q.pres ? 3 : 2;
+    if (total > 0)
+        CUDA_TRY(c, cudaMemcpyAsync(indices, dind, sizeof(int64_t) * total, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaFreeAsync(dptr, st));
+    CUDA_TRY(c, cudaFreeAsync(dind, st));
+    if (inv) CUDA_TRY(c, cudaFreeAsync(inv, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    return CG_OK;
+}
+
+static int neighbor_check(cg_context *c, double radius)
+{
+    if (!c->grid_current || c->n != c->n_owned)
+        return fail(c, CG_ERR_STATE, "no grid over the stored positions: call cg_build_grid first");
+    if (!(radius > 0)) return fail(c, CG_ERR_VALUE, "radius must be positive, got %g", radius);
+    if (radius > c->geo.L)
+        return fail(c, CG_ERR_STENCIL, "radius %g exceeds box_length %g", radius, c->geo.L);
+    return CG_OK;
+}
+
+extern "C" {
+
+int cg_neighbor_counts(cg_context *c, double radius, int64_t *counts)
+{
+    if (!c || !counts) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    int rc = neighbor_check(c, radius);
+    if (rc || c->n == 0) return rc;
+    return c->prec == CG_FP64 ? neighbor_query_t<double>(c, radius, counts, nullptr, nullptr)
+                              : neighbor_query_t<float>(c, radius, counts, nullptr, nullptr);
+}
+
+int cg_neighbor_fill(cg_context *c, double radius, const int64_t *indptr, int64_t *indices)
+{
+    if (!c || !indptr) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    int rc = neighbor_check(c, radius);
+    if (rc || c->n == 0) return rc;
+    return c->prec == CG_FP64 ? neighbor_query_t<double>(c, radius, nullptr, indptr, indices)
+                              : neighbor_query_t<float>(c, radius, nullptr, indptr, indices);
+}
+
+}  // extern "C"
+
 
