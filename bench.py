@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "gloo"],
                     help="multi-GPU exchange (gloo: host-staged, e.g. several ranks on one GPU)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (testing)")
+    ap.add_argument("--force-slab", action="store_true",
+                    help="run the slab (multi-GPU) driver even at world size 1 (exercises the exchange)")
     return ap.parse_args()
 
 
@@ -183,9 +185,14 @@ def dist_init(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.same_device:
         local = 0
-    if world > 1:
+    if world > 1 or (args.force_slab and args.impl == "ours"):
         import torch
         import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(local)
         if args.exchange == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -341,7 +348,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    if world > 1 or args.force_slab:
         main_slab(args, rank, world, local)
         return
     import torch

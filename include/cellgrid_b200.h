@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CG_ABI_VERSION 3
+#define CG_ABI_VERSION 4
 
 /* status codes */
 #define CG_OK 0
@@ -143,13 +143,14 @@ int cg_neighbor_fill(cg_context *ctx, double radius, const int64_t *indptr, int6
 
 /* ---- x-slab decomposition (multi-GPU).  The reference has no
  * distributed layer: these entry points carry the same step across ranks,
- * one context per GPU.  Device buffers (send/recv) are raw device pointers
- * owned by the caller (e.g. torch CUDA tensors handed to NCCL); records are
- * cg_record_bytes() each.  Per step, on every rank:
+ * one context per GPU.  Rank r owns the agents whose global box plane lies in
+ * [X_r, X_r+1), X_k = floor(k dimx / world), and sees planes X_r - 1 and
+ * X_r+1 as ghosts.  Device buffers (send/recv) are raw device pointers owned
+ * by the caller (e.g. torch CUDA tensors handed to NCCL); records are
+ * cg_record_bytes() each.  Per step, on every rank, ONE exchange round:
  *   cg_local_bbox -> all-reduce (min/min/min/max/max/max/max) -> cg_slab_plan
- *   -> all-to-all counts -> cg_slab_migrate(send) -> all-to-all records ->
- *   cg_slab_accept(recv) -> cg_slab_halo(NULL) / cg_slab_halo(send) ->
- *   exchange with rank-1 / rank+1 -> cg_slab_set_ghosts(recv) -> cg_slab_step.
+ *   -> all-to-all of the 3-per-rank counts -> cg_slab_pack(send) ->
+ *   all-to-all of the records -> cg_slab_unpack(recv) -> cg_slab_step.
  * Owned agents' results are those of a single-GPU step over the global pool. */
 int64_t cg_record_bytes(const cg_context *ctx);
 /* Pre-size the agent buffers (before cg_upload) for arrivals and ghosts. */
@@ -157,20 +158,20 @@ int cg_reserve(cg_context *ctx, int64_t capacity);
 /* Exact bbox of the owned agents (min xyz, max xyz) + max diameter. */
 int cg_local_bbox(cg_context *ctx, double out[7]);
 /* Geometry from the global bbox (spatial.py:99-116; GridOverflowError as
- * cg_step), slab planes X_k = floor(k dimx / world): planes = {X_rank,
- * X_rank+1}; counts[k] = owned agents whose box plane rank k owns. */
+ * cg_step) and slab planes: planes = {X_rank, X_rank+1}.  counts (3 * world):
+ * for destination rank q, counts[3q] = owned agents that migrate to q (0 for
+ * q == rank), counts[3q+1] = owned agents in plane X_q - 1 (q's lo ghosts),
+ * counts[3q+2] = owned agents in plane X_q+1 (q's hi ghosts). */
 int cg_slab_plan(cg_context *ctx, const double bbox[7], double interaction_radius, int64_t box_cap,
                  int world, int rank, int64_t *counts, int64_t planes[2]);
-/* Departing agents -> send (grouped by destination rank, ascending, own rank
- * skipped); the remaining agents are compacted. */
-int cg_slab_migrate(cg_context *ctx, void *send);
-/* Append count received records as owned agents. */
-int cg_slab_accept(cg_context *ctx, const void *recv, int64_t count);
-/* send == NULL: counts[0] / counts[1] = owned agents in plane X_rank (for
- * rank-1) / plane X_rank+1 - 1 (for rank+1); else pack them in that order. */
-int cg_slab_halo(cg_context *ctx, void *send, int64_t counts[2]);
-/* This step's ghosts (candidates only, dropped after cg_slab_step). */
-int cg_slab_set_ghosts(cg_context *ctx, const void *recv, int64_t count);
+/* Outgoing records -> send, grouped by destination rank (ascending), each
+ * destination's run = [migrants][lo ghosts][hi ghosts] with the cg_slab_plan
+ * counts; then the migrants leave the owned set (compacted). */
+int cg_slab_pack(cg_context *ctx, void *send);
+/* recv = the runs received from every source rank (ascending), run sizes
+ * recv_counts[3s .. 3s+2] as in cg_slab_plan: migrants join the owned set,
+ * ghosts are this step's candidates (dropped after cg_slab_step). */
+int cg_slab_unpack(cg_context *ctx, const void *recv, const int64_t *recv_counts);
 /* The mechanical step on the owned agents over the slab's sub-grid. */
 int cg_slab_step(cg_context *ctx, const double params[5], int flags, cg_step_stats *stats);
 

@@ -29,8 +29,8 @@ EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_
             "cg_fetch_stats", "cg_build_grid", "cg_synchronize", "cg_grid_export",
             "cg_record_export", "cg_box_ids", "cg_force_phase", "cg_launch_count",
             "cg_host_alloc", "cg_host_free", "cg_record_bytes", "cg_reserve", "cg_local_bbox",
-            "cg_slab_plan", "cg_slab_migrate", "cg_slab_accept", "cg_slab_halo",
-            "cg_slab_set_ghosts", "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill")
+            "cg_slab_plan", "cg_slab_pack", "cg_slab_unpack",
+            "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill")
 
 
 class GridOverflowError(RuntimeError):
@@ -103,17 +103,15 @@ def load():
         "cg_local_bbox": ([_P, _P], ctypes.c_int),
         "cg_slab_plan": ([_P, _P, ctypes.c_double, _I64, ctypes.c_int, ctypes.c_int, _P, _P],
                          ctypes.c_int),
-        "cg_slab_migrate": ([_P, _P], ctypes.c_int),
-        "cg_slab_accept": ([_P, _P, _I64], ctypes.c_int),
-        "cg_slab_halo": ([_P, _P, _P], ctypes.c_int),
-        "cg_slab_set_ghosts": ([_P, _P, _I64], ctypes.c_int),
+        "cg_slab_pack": ([_P, _P], ctypes.c_int),
+        "cg_slab_unpack": ([_P, _P, _P], ctypes.c_int),
         "cg_slab_step": ([_P, _P, ctypes.c_int, ctypes.POINTER(StepStatsC)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
-    if L.cg_abi_version() != 3:
+    if L.cg_abi_version() != 4:
         raise NativeUnavailable("ABI version mismatch")
     _lib = L
     return L
@@ -257,33 +255,23 @@ class Context:
         return out
 
     def slab_plan(self, bbox, world, rank, interaction_radius=None, box_cap=1 << 24):
+        """-> (counts[3 * world], planes[2]); see cg_slab_plan."""
         bb = np.ascontiguousarray(bbox, np.float64)
-        counts = np.zeros(world, np.int64)
+        counts = np.zeros(3 * world, np.int64)
         planes = np.zeros(2, np.int64)
         ir = float("nan") if interaction_radius is None else float(interaction_radius)
         check(load().cg_slab_plan(self.h, ptr(bb), ir, int(box_cap), int(world), int(rank),
                                   ptr(counts), ptr(planes)), self.h)
         return counts, planes
 
-    def slab_migrate(self, send_ptr):
-        check(load().cg_slab_migrate(self.h, send_ptr), self.h)
+    def slab_pack(self, send_ptr):
+        check(load().cg_slab_pack(self.h, send_ptr), self.h)
         self.n = int(load().cg_count(self.h))
 
-    def slab_accept(self, recv_ptr, count):
-        check(load().cg_slab_accept(self.h, recv_ptr, int(count)), self.h)
+    def slab_unpack(self, recv_ptr, recv_counts):
+        rc = np.ascontiguousarray(recv_counts, np.int64)
+        check(load().cg_slab_unpack(self.h, recv_ptr, ptr(rc)), self.h)
         self.n = int(load().cg_count(self.h))
-
-    def slab_halo_counts(self):
-        counts = np.zeros(2, np.int64)
-        check(load().cg_slab_halo(self.h, None, ptr(counts)), self.h)
-        return counts
-
-    def slab_halo_pack(self, send_ptr):
-        counts = np.zeros(2, np.int64)
-        check(load().cg_slab_halo(self.h, send_ptr, ptr(counts)), self.h)
-
-    def slab_set_ghosts(self, recv_ptr, count):
-        check(load().cg_slab_set_ghosts(self.h, recv_ptr, int(count)), self.h)
 
     def slab_step(self, params5, flags=0, wait=True):
         p = np.ascontiguousarray(params5, np.float64)

@@ -70,6 +70,7 @@ struct Buffers {
     Proxies P() const { return Proxies{prox}; }
     int64_t pairs = 0;
     void *stage = nullptr;           // download staging (n x 8 B)
+    int64_t head = 0;                // front headroom (elements) of rec / adh / uid
 };
 
 }  // namespace
@@ -111,6 +112,8 @@ struct cg_context {
     bool last_record = false;
     bool last_dense = false;
     bool grid_current = false;    // the grid indexes the stored positions (cg_build_grid)
+    int rot = 0;                  // relaid slab sub-grid: slot s lives at storage s - rot (lo ghosts in
+                                  // the buffers' front headroom, owned agents at [0, n_owned))
     int64_t sort_steps = 0;
     Geometry geo_sort{};          // geometry of the last sort step (presentation order)
     // options
@@ -124,15 +127,17 @@ struct cg_context {
         Geometry g{};            // global geometry of this step
         SlabBounds B{};
         int rank = 0, world = 1, x0 = 0, x1 = 0;
-        unsigned char *dest = nullptr;
-        int *dep = nullptr, *holes = nullptr, *movers = nullptr, *lo = nullptr, *hi = nullptr;
+        bool packed = false;
+        unsigned char *dest = nullptr;           // owner rank | ghost flags (slab.cuh)
+        int *out = nullptr, *holes = nullptr, *movers = nullptr;
         unsigned *cnt = nullptr;                 // 8 counters
-        unsigned long long *counts = nullptr;    // per destination rank
-        unsigned long long *dest_off = nullptr;
+        unsigned long long *counts = nullptr;    // kHist bins (slab.cuh)
+        unsigned long long *seg_off = nullptr;   // send-buffer run starts, 3 per destination
         unsigned *cursor = nullptr;
         int64_t cap = 0;
-        int64_t h_counts[kMaxWorld] = {};
-        unsigned h_halo[2] = {0, 0};
+        int64_t h_counts[kHist] = {};
+        int64_t steps = 0;
+        int64_t ghost_lo = 0;    // ghosts from rank - 1 (in front of the ghost buffer)
     } slab;
     std::string err;
 };
@@ -161,8 +166,12 @@ static int fail(cg_context *c, int code, const char *fmt, ...)
 static void free_agents(cg_context *c)
 {
     Buffers &b = c->b;
-    void *ptrs[] = {b.rec[0], b.rec[1], b.adh[0], b.adh[1], b.uid[0], b.uid[1],
-                    b.disp[0], b.disp[1], b.disp[2], b.key_rank, b.tmp, b.idx, b.skey, b.pres,
+    for (int k = 0; k < 2; ++k) {
+        if (b.rec[k]) cudaFree((char *)b.rec[k] - 4 * c->esz * b.head);
+        if (b.adh[k]) cudaFree((char *)b.adh[k] - c->esz * b.head);
+        if (b.uid[k]) cudaFree(b.uid[k] - b.head);
+    }
+    void *ptrs[] = {b.disp[0], b.disp[1], b.disp[2], b.key_rank, b.tmp, b.idx, b.skey, b.pres,
                     b.rec_m, b.rec_nk, b.prox, b.stage, b.pkey[0], b.pkey[1], b.pscratch, b.ovf};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -175,10 +184,17 @@ static int alloc_agents(cg_context *c, int64_t cap)
     free_agents(c);
     Buffers &b = c->b;
     const size_t fe = c->esz * (size_t)cap, ie = sizeof(int) * (size_t)cap;
+    // front headroom: a relaid slab step stores its lo ghosts before element 0
+    const int64_t H = cap / 16 + 1024;
     for (int k = 0; k < 2; ++k) {
-        CUDA_TRY(c, cudaMalloc(&b.rec[k], 4 * fe));
-        CUDA_TRY(c, cudaMalloc(&b.adh[k], fe));
-        CUDA_TRY(c, cudaMalloc(&b.uid[k], sizeof(uint64_t) * (size_t)cap));
+        void *p;
+        CUDA_TRY(c, cudaMalloc(&p, 4 * c->esz * (size_t)(cap + H)));
+        b.rec[k] = (char *)p + 4 * c->esz * H;
+        CUDA_TRY(c, cudaMalloc(&p, c->esz * (size_t)(cap + H)));
+        b.adh[k] = (char *)p + c->esz * H;
+        CUDA_TRY(c, cudaMalloc(&p, sizeof(uint64_t) * (size_t)(cap + H)));
+        b.uid[k] = (uint64_t *)p + H;
+        b.head = H;
     }
     for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMalloc(&b.disp[a], fe));
     CUDA_TRY(c, cudaMalloc(&b.key_rank, sizeof(int2) * (size_t)cap));
@@ -382,7 +398,7 @@ static int materialize_presentation(cg_context *c)
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
 // idx (or, when relayout, the records in slot order in the alternate buffers).
 template <typename T>
-static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort);
+static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort, int rot = 0);
 
 template <typename T>
 static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, bool sort,
@@ -402,7 +418,7 @@ static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, 
 
 // Grid rebuild for a given geometry (global, or a slab's sub-grid).
 template <typename T>
-static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort)
+static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort, int rot)
 {
     const int n = (int)c->n;
     cudaStream_t st = c->stream;
@@ -432,8 +448,8 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
             // pkey carries the last sort step's box (this step's on a sort step)
             place_relayout<T><<<nblk, kThreads, 0, st>>>(
                 n, g, c->bd, c->b.key_rank, c->offset, rec, (T *)c->b.adh[a], c->b.uid[a], c->b.skey, c->b.P(),
-                sort ? nullptr : c->b.pkey[a], c->b.pkey[oa], (Rec<T> *)c->b.rec[o], (T *)c->b.adh[oa],
-                c->b.uid[oa]);
+                sort ? nullptr : c->b.pkey[a], rot ? nullptr : c->b.pkey[oa], (Rec<T> *)c->b.rec[o] - rot,
+                (T *)c->b.adh[oa] - rot, c->b.uid[oa] - rot);
             LAUNCH_CHECK(c);
             c->launches += 1;
             CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
@@ -452,8 +468,8 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
         if (relayout) {
             order_gather<T, true><<<nblk, kThreads, 0, st>>>(
                 n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, rec, (T *)c->b.adh[a], c->b.uid[a],
-                c->b.skey, c->b.P(), nullptr, (Rec<T> *)c->b.rec[o], (T *)c->b.adh[oa], c->b.uid[oa],
-                sort ? c->b.pkey[oa] : nullptr);
+                c->b.skey, c->b.P(), nullptr, (Rec<T> *)c->b.rec[o] - rot, (T *)c->b.adh[oa] - rot,
+                c->b.uid[oa] - rot, sort ? c->b.pkey[oa] : nullptr);
         } else {
             order_gather<T, false><<<nblk, kThreads, 0, st>>>(
                 n, g, c->bd, c->b.tmp, c->b.key_rank, c->offset, rec, (T *)c->b.adh[a], c->b.uid[a],
@@ -470,6 +486,7 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
     } else {
         c->relaid = false;
     }
+    c->rot = relayout ? rot : 0;
     if (sort) c->geo_sort = g;
     c->have_grid = true;
     return CG_OK;
@@ -583,21 +600,24 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     A.skey = c->b.skey;
     A.idx = c->relaid ? nullptr : c->b.idx;
     A.off = c->offset;
-    A.rec = (const Rec<T> *)c->b.rec[cp];
-    A.adh = (const T *)c->b.adh[ca];
-    A.uid = c->b.uid[ca];
+    // relaid slab sub-grid: every storage-order column is addressed by slot
+    // (shifted by rot; the writes land at [0, n_owned))
+    const int rot = c->relaid ? c->rot : 0;
+    A.rec = (const Rec<T> *)c->b.rec[cp] - rot;
+    A.adh = (const T *)c->b.adh[ca] - rot;
+    A.uid = c->b.uid[ca] - rot;
     A.p = P;
     A.rmax = nextafterf((float)(0.5 * c->max_diam), INFINITY);
     // fp32 prefilter margin: every stored / derived fp32 coordinate is within
     // a few ulp of E (box-local x/y, grid-relative z); 64 ulp(E) is used
     const double E = c->geo.L * (double)std::max(3, std::max(c->geo.dimz + 2, 3));
     A.margin = (float)(64.0 * E * 5.9604644775390625e-8);
-    A.disp_x = (T *)c->b.disp[0];
-    A.disp_y = (T *)c->b.disp[1];
-    A.disp_z = (T *)c->b.disp[2];
-    A.new_rec = nrec;
-    A.rec_m = record ? c->b.rec_m : nullptr;
-    A.rec_nk = record ? c->b.rec_nk : nullptr;
+    A.disp_x = (T *)c->b.disp[0] - rot;
+    A.disp_y = (T *)c->b.disp[1] - rot;
+    A.disp_z = (T *)c->b.disp[2] - rot;
+    A.new_rec = nrec ? nrec - rot : nullptr;
+    A.rec_m = record ? c->b.rec_m - rot : nullptr;
+    A.rec_nk = record ? c->b.rec_nk - rot : nullptr;
     A.slots = c->slots;
     // bbox shell (see sweep7.cuh): an agent can only become extreme if it ends
     // within max_displacement (+ rounding slack) of the old bbox faces
@@ -615,6 +635,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     A.ovf = c->b.ovf;
     A.ovf_count = c->ovf_count;
     A.n_owned = (int)c->n_owned;
+    A.own_lo = c->rot;
     int rc = launch_sweep7<T>(c, A);
     if (rc) return rc;
     unsigned long long *stat = c->stat_dev + (c->steps_done % kRing) * kStatSlots;
@@ -731,17 +752,17 @@ static int slab_alloc(cg_context *c)
 {
     auto &S = c->slab;
     if (S.cap >= c->cap && S.cnt) return CG_OK;
-    void *ptrs[] = {S.dest, S.dep, S.holes, S.movers, S.lo, S.hi, S.cnt, S.counts, S.dest_off, S.cursor};
+    void *ptrs[] = {S.dest, S.out, S.holes, S.movers, S.cnt, S.counts, S.seg_off, S.cursor};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     const size_t n = (size_t)std::max<int64_t>(c->cap, 1);
     CUDA_TRY(c, cudaMalloc(&S.dest, n));
-    int **ints[] = {&S.dep, &S.holes, &S.movers, &S.lo, &S.hi};
+    int **ints[] = {&S.out, &S.holes, &S.movers};
     for (int **p : ints) CUDA_TRY(c, cudaMalloc(p, sizeof(int) * n));
     CUDA_TRY(c, cudaMalloc(&S.cnt, sizeof(unsigned) * 8));
-    CUDA_TRY(c, cudaMalloc(&S.counts, sizeof(unsigned long long) * kMaxWorld));
-    CUDA_TRY(c, cudaMalloc(&S.dest_off, sizeof(unsigned long long) * kMaxWorld));
-    CUDA_TRY(c, cudaMalloc(&S.cursor, sizeof(unsigned) * kMaxWorld));
+    CUDA_TRY(c, cudaMalloc(&S.counts, sizeof(unsigned long long) * kHist));
+    CUDA_TRY(c, cudaMalloc(&S.seg_off, sizeof(unsigned long long) * kHist));
+    CUDA_TRY(c, cudaMalloc(&S.cursor, sizeof(unsigned) * kHist));
     S.cap = c->cap;
     return CG_OK;
 }
@@ -787,50 +808,59 @@ static int slab_plan_t(cg_context *c, const double bb[7], double ir, int64_t box
             return fail(c, CG_ERR_GRID_OVERFLOW, "slab sub-grid of %lld boxes exceeds cap %lld",
                         (long long)sub, (long long)box_cap);
     }
+    // every candidate radius is bounded by the global largest diameter
+    c->max_diam = std::max(c->max_diam, bb[6]);
     planes[0] = S.x0;
     planes[1] = S.x1;
     cudaStream_t st = c->stream;
-    CUDA_TRY(c, cudaMemsetAsync(S.counts, 0, sizeof(unsigned long long) * kMaxWorld, st));
+    CUDA_TRY(c, cudaMemsetAsync(S.counts, 0, sizeof(unsigned long long) * kHist, st));
     const int n = (int)c->n_owned;
     if (n > 0) {
-        slab_dest<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, g, S.B, (const Rec<T> *)c->b.rec[c->cur_pos], S.dest,
-                                                              S.counts);
+        slab_dest<T><<<std::min(cdiv(n, kThreads), 148 * 8), kThreads, 0, st>>>(
+            n, g, S.B, rank, (const Rec<T> *)c->b.rec[c->cur_pos], S.dest, S.counts);
         LAUNCH_CHECK(c);
         c->launches += 1;
     }
-    unsigned long long h[kMaxWorld];
-    CUDA_TRY(c, cudaMemcpyAsync(h, S.counts, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, st));
+    unsigned long long h[kHist];
+    CUDA_TRY(c, cudaMemcpyAsync(h, S.counts, sizeof(unsigned long long) * (3 * world + 1), cudaMemcpyDeviceToHost,
+                                st));
     CUDA_TRY(c, cudaStreamSynchronize(st));
-    for (int k = 0; k < world; ++k) counts[k] = S.h_counts[k] = (int64_t)h[k];
+    for (int k = 0; k <= 3 * world; ++k) S.h_counts[k] = (int64_t)h[k];
+    for (int k = 0; k < 3 * world; ++k) counts[k] = S.h_counts[k];
     S.planned = true;
+    S.packed = false;
     return CG_OK;
 }
 
 template <typename T>
-static int slab_migrate_t(cg_context *c, void *send)
+static int slab_pack_t(cg_context *c, void *send)
 {
     auto &S = c->slab;
     const int n = (int)c->n_owned;
-    const int64_t stay = S.h_counts[S.rank];
-    const int ndep = (int)(n - stay);
-    if (ndep == 0) return CG_OK;
-    cudaStream_t st = c->stream;
-    unsigned long long off[kMaxWorld];
+    const int W = S.world;
+    const int n_keep = (int)S.h_counts[3 * W];
+    unsigned long long off[kHist];
     unsigned long long acc = 0;
-    for (int k = 0; k < S.world; ++k) {
+    for (int k = 0; k < 3 * W; ++k) {
         off[k] = acc;
-        if (k != S.rank) acc += (unsigned long long)S.h_counts[k];
+        acc += (unsigned long long)S.h_counts[k];
     }
-    CUDA_TRY(c, cudaMemcpyAsync(S.dest_off, off, sizeof(unsigned long long) * S.world, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(c, cudaMemsetAsync(S.cursor, 0, sizeof(unsigned) * kMaxWorld, st));
+    S.packed = true;
+    if (acc == 0 && n_keep == n) return CG_OK;
+    cudaStream_t st = c->stream;
+    CUDA_TRY(c, cudaMemcpyAsync(S.seg_off, off, sizeof(unsigned long long) * 3 * W, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(c, cudaMemsetAsync(S.cursor, 0, sizeof(unsigned) * 3 * W, st));
     CUDA_TRY(c, cudaMemsetAsync(S.cnt, 0, sizeof(unsigned) * 8, st));
-    const int n_keep = (int)stay;
-    slab_lists<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, n_keep, S.rank, S.dest, S.dep, S.holes, S.movers, S.cnt);
+    slab_lists<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, n_keep, S.rank, S.dest, S.out, S.holes, S.movers, S.cnt);
+    unsigned hc[3];
+    CUDA_TRY(c, cudaMemcpyAsync(hc, S.cnt, sizeof hc, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
     const SlabCols<T> C = cur_cols<T>(c);
-    slab_pack<T><<<cdiv(ndep, kThreads), kThreads, 0, st>>>(ndep, S.dep, S.dest, S.dest_off, S.cursor, C,
-                                                             (SlabRecord<T> *)send);
-    // |holes| = departures below n_keep <= ndep; the kernel reads the count on device
-    slab_fill_holes_dev<T><<<cdiv(ndep, kThreads), kThreads, 0, st>>>(S.cnt + 1, S.holes, S.movers, C);
+    if (hc[0])
+        slab_pack_out<T><<<cdiv(hc[0], kThreads), kThreads, 0, st>>>((int)hc[0], S.rank, S.out, S.dest, S.seg_off,
+                                                                     S.cursor, C, (SlabRecord<T> *)send);
+    if (hc[1])
+        slab_fill_holes<T><<<cdiv(hc[1], kThreads), kThreads, 0, st>>>((int)hc[1], S.holes, S.movers, C);
     LAUNCH_CHECK(c);
     c->launches += 3;
     CUDA_TRY(c, cudaStreamSynchronize(st));   // the send buffer is handed to the exchange
@@ -840,63 +870,48 @@ static int slab_migrate_t(cg_context *c, void *send)
 }
 
 template <typename T>
-static int slab_unpack_t(cg_context *c, const void *recv, int64_t count, bool ghosts)
-{
-    if (count <= 0) return CG_OK;
-    const int64_t base = ghosts ? c->n_owned : c->n_owned;
-    if (base + count > c->cap)
-        return fail(c, CG_ERR_POOL_CAPACITY, "slab needs %lld agents, capacity %lld (cg_reserve)",
-                    (long long)(base + count), (long long)c->cap);
-    cudaStream_t st = c->stream;
-    slab_unpack<T><<<cdiv(count, kThreads), kThreads, 0, st>>>((int)count, (int)base, (const SlabRecord<T> *)recv,
-                                                                cur_cols<T>(c), ghosts ? nullptr : c->maxd_enc);
-    LAUNCH_CHECK(c);
-    c->launches += 1;
-    if (ghosts) {
-        c->n = base + count;
-    } else {
-        unsigned long long enc = 0;
-        CUDA_TRY(c, cudaMemcpyAsync(&enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(c, cudaStreamSynchronize(st));
-        c->max_diam = dec_ordered(enc);
-        c->n = c->n_owned = base + count;
-        c->bbox_valid = false;
-    }
-    return CG_OK;
-}
-
-template <typename T>
-static int slab_halo_t(cg_context *c, void *send, int64_t counts[2])
+static int slab_unpack_t(cg_context *c, const void *recv, const int64_t *rc3)
 {
     auto &S = c->slab;
-    cudaStream_t st = c->stream;
-    const int n = (int)c->n_owned;
-    if (!send) {
-        CUDA_TRY(c, cudaMemsetAsync(S.cnt, 0, sizeof(unsigned) * 8, st));
-        const int lo_plane = S.rank > 0 ? S.x0 : -2, hi_plane = S.rank < S.world - 1 ? S.x1 - 1 : -2;
-        if (n > 0) {
-            slab_halo_list<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, S.g, lo_plane, hi_plane,
-                                                                       (const Rec<T> *)c->b.rec[c->cur_pos], S.lo,
-                                                                       S.hi, S.cnt);
-            LAUNCH_CHECK(c);
-            c->launches += 1;
-        }
-        CUDA_TRY(c, cudaMemcpyAsync(S.h_halo, S.cnt, sizeof(unsigned) * 2, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(c, cudaStreamSynchronize(st));
-        counts[0] = S.h_halo[0];
-        counts[1] = S.h_halo[1];
-        return CG_OK;
+    const int W = S.world;
+    int64_t mig = 0, glo = 0, ghi = 0;
+    for (int s = 0; s < W; ++s) {
+        if (rc3[3 * s] < 0 || rc3[3 * s + 1] < 0 || rc3[3 * s + 2] < 0)
+            return fail(c, CG_ERR_VALUE, "negative receive count");
+        mig += rc3[3 * s];
+        glo += rc3[3 * s + 1];
+        ghi += rc3[3 * s + 2];
     }
-    const SlabCols<T> C = cur_cols<T>(c);
-    SlabRecord<T> *out = (SlabRecord<T> *)send;
-    if (S.h_halo[0])
-        slab_gather_records<T><<<cdiv(S.h_halo[0], kThreads), kThreads, 0, st>>>((int)S.h_halo[0], S.lo, C, out);
-    if (S.h_halo[1])
-        slab_gather_records<T><<<cdiv(S.h_halo[1], kThreads), kThreads, 0, st>>>((int)S.h_halo[1], S.hi, C,
-                                                                               out + S.h_halo[0]);
-    LAUNCH_CHECK(c);
-    c->launches += 2;
-    CUDA_TRY(c, cudaStreamSynchronize(st));
+    const int64_t base = c->n_owned, total = mig + glo + ghi;
+    if (base + total > c->cap)
+        return fail(c, CG_ERR_POOL_CAPACITY, "slab needs %lld agents, capacity %lld (cg_reserve)",
+                    (long long)(base + total), (long long)c->cap);
+    // destination of every run: migrants after the owned set, then lo ghosts, then hi ghosts
+    SlabSegs G{};
+    int64_t pos = 0, dm = base, dl = base + mig, dh = base + mig + glo;
+    for (int s = 0; s < W; ++s)
+        for (int kind = 0; kind < 3; ++kind) {
+            const int k = 3 * s + kind;
+            G.start[k] = pos;
+            const int64_t cnt = rc3[k];
+            int64_t &d = kind == 0 ? dm : kind == 1 ? dl : dh;
+            G.dst[k] = (int)d;
+            d += cnt;
+            pos += cnt;
+        }
+    G.nseg = 3 * W;
+    G.start[3 * W] = pos;
+    if (total > 0) {
+        cudaStream_t st = c->stream;
+        slab_unpack_segs<T><<<cdiv(total, kThreads), kThreads, 0, st>>>((int)total, G, (const SlabRecord<T> *)recv,
+                                                                        cur_cols<T>(c));
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+    }
+    c->n_owned = base + mig;
+    c->n = base + total;
+    if (mig) c->bbox_valid = false;
+    S.ghost_lo = glo;
     return CG_OK;
 }
 
@@ -904,7 +919,7 @@ template <typename T>
 static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t *step_id)
 {
     auto &S = c->slab;
-    if (!S.planned) return fail(c, CG_ERR_STATE, "cg_slab_step without cg_slab_plan");
+    if (!S.planned || !S.packed) return fail(c, CG_ERR_STATE, "cg_slab_step without cg_slab_plan / cg_slab_pack");
     const int slot = (int)(c->steps_done % kRing);
     cg_step_stats &St = c->ring[slot];
     std::memset(&St, 0, sizeof St);
@@ -925,7 +940,13 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
     const bool freeze = (flags & CG_STEP_FREEZE) != 0;
     const bool record = (flags & CG_STEP_RECORD) != 0;
     if (c->n > 0) {
-        if ((rc = build_grid_geo<T>(c, g, false, false))) return rc;
+        // relaid storage as in the single-context step; the owned planes are
+        // the middle slot range, rotated to the front by the lo-ghost count
+        // (the first slot of local plane 1 when a lo ghost plane exists)
+        const bool relayout = c->sweep_impl == 1 && c->n > 1 && (S.steps % c->relayout_every == 0);
+        const int rot = xl == S.x0 - 1 ? (int)S.ghost_lo : 0;
+        if ((rc = build_grid_geo<T>(c, g, relayout && rot <= c->b.head, false, rot))) return rc;
+        S.steps++;
         CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
         if ((rc = run_sweep<T>(c, params, freeze, record))) return rc;
         if (!freeze) c->cur_pos = 1 - c->cur_pos;
@@ -950,7 +971,7 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
     c->have_grid = false;   // the sub-grid is not exportable
     c->pres_state = PRES_IDENTITY;
     c->steps_done++;
-    S.planned = false;
+    S.planned = S.packed = false;
     return CG_OK;
 }
 
@@ -1425,37 +1446,22 @@ int cg_slab_plan(cg_context *c, const double bbox[7], double interaction_radius,
                               : slab_plan_t<float>(c, bbox, interaction_radius, box_cap, world, rank, counts, planes);
 }
 
-int cg_slab_migrate(cg_context *c, void *send)
+int cg_slab_pack(cg_context *c, void *send)
 {
     if (!c) return CG_ERR_VALUE;
-    if (!c->slab.planned) return fail(c, CG_ERR_STATE, "cg_slab_migrate without cg_slab_plan");
     CUDA_TRY(c, cudaSetDevice(c->device));
-    return c->prec == CG_FP64 ? slab_migrate_t<double>(c, send) : slab_migrate_t<float>(c, send);
+    if (!c->slab.planned || c->slab.packed) return fail(c, CG_ERR_STATE, "cg_slab_pack needs a fresh cg_slab_plan");
+    return c->prec == CG_FP64 ? slab_pack_t<double>(c, send) : slab_pack_t<float>(c, send);
 }
 
-int cg_slab_accept(cg_context *c, const void *recv, int64_t count)
+int cg_slab_unpack(cg_context *c, const void *recv, const int64_t *recv_counts)
 {
-    if (!c) return CG_ERR_VALUE;
+    if (!c || !recv_counts) return CG_ERR_VALUE;
     CUDA_TRY(c, cudaSetDevice(c->device));
-    return c->prec == CG_FP64 ? slab_unpack_t<double>(c, recv, count, false)
-                              : slab_unpack_t<float>(c, recv, count, false);
-}
-
-int cg_slab_halo(cg_context *c, void *send, int64_t counts[2])
-{
-    if (!c) return CG_ERR_VALUE;
-    if (!c->slab.planned) return fail(c, CG_ERR_STATE, "cg_slab_halo without cg_slab_plan");
-    CUDA_TRY(c, cudaSetDevice(c->device));
-    return c->prec == CG_FP64 ? slab_halo_t<double>(c, send, counts) : slab_halo_t<float>(c, send, counts);
-}
-
-int cg_slab_set_ghosts(cg_context *c, const void *recv, int64_t count)
-{
-    if (!c) return CG_ERR_VALUE;
-    CUDA_TRY(c, cudaSetDevice(c->device));
-    c->n = c->n_owned;
-    return c->prec == CG_FP64 ? slab_unpack_t<double>(c, recv, count, true)
-                              : slab_unpack_t<float>(c, recv, count, true);
+    if (!c->slab.packed) return fail(c, CG_ERR_STATE, "cg_slab_unpack without cg_slab_pack");
+    if (c->n != c->n_owned) return fail(c, CG_ERR_STATE, "cg_slab_unpack called twice");
+    return c->prec == CG_FP64 ? slab_unpack_t<double>(c, recv, recv_counts)
+                              : slab_unpack_t<float>(c, recv, recv_counts);
 }
 
 int cg_slab_step(cg_context *c, const double params[5], int flags, cg_step_stats *stats)

@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(kThreads) scan_lookback(int nb, int *__restric
 }
 
 // ---------------------------------------------------------------- K4 place/order
+
 __global__ void __launch_bounds__(kThreads) place(int n, const int2 *__restrict__ key_rank,
                                                   const int *__restrict__ offset, int *__restrict__ tmp)
 {

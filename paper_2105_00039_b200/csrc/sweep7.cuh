@@ -58,7 +58,16 @@ struct Sweep7Args {
     int *ovf;                   // slots of agents deferred to the overflow kernel
     unsigned *ovf_count;
     int n_owned;                // storage indices >= n_owned are ghosts (slab halo): not targets
+    int own_lo;                 // targets are storage indices [own_lo, own_lo + n_owned): a relaid
+                                // slab sub-grid keeps its lo ghosts in front of the owned agents
 };
+
+// slot -> storage index: the idx map, or the slot itself (relaid storage)
+template <typename A_t>
+__device__ __forceinline__ int storage_of(const A_t &A, int s)
+{
+    return A.idx ? __ldg(A.idx + s) : s;
+}
 
 // packed fp32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2)
 typedef unsigned long long f32x2;
@@ -109,8 +118,8 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         const int key = __ldg(A.skey + s);
         int ix, iy, iz;
         decode_box(A.bd, key, ix, iy, iz);
-        const int a = A.idx ? __ldg(A.idx + s) : s;
-        if (a >= A.n_owned) return;   // a ghost: candidate only
+        const int a = storage_of(A, s);
+        if ((unsigned)(a - A.own_lo) >= (unsigned)A.n_owned) return;   // a ghost: candidate only
         const T half = T(0.5), zero = A.p.zero;
         const float *myp = A.prox.p + 8 * (s >> 1) + (s & 1);
         const float mex = __ldg(myp), mey = __ldg(myp + 2), mez = __ldg(myp + 4);
@@ -201,7 +210,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             int p = 0;
             if (p < cnt_ && LST(p) == s) ++p;
             if (p >= cnt_) return;
-            int j = A.idx ? __ldg(A.idx + LST(p)) : LST(p);
+            int j = storage_of(A, LST(p));
             Rec<T> o = A.rec[j];
 #pragma unroll 1
             while (p < cnt_) {
@@ -210,7 +219,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 ++p;
                 if (p < cnt_ && LST(p) == s) ++p;   // the agent itself
                 if (p < cnt_) {
-                    j = A.idx ? __ldg(A.idx + LST(p)) : LST(p);
+                    j = storage_of(A, LST(p));
                     o = A.rec[j];
                 }
                 const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;   // kernels.py:198-203
@@ -282,7 +291,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 evaluate(ns);
             }
         } else {
-            auto cand_uid = [&](int t) -> uint64_t { return A.uid[A.idx ? __ldg(A.idx + t) : t]; };
+            auto cand_uid = [&](int t) -> uint64_t { return A.uid[storage_of(A, t)]; };
             // first walk: keep the first KS survivors, count all of them
             int ns = 0, total = 0;
             m = walk(

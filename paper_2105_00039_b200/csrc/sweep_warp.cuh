@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
     const float Lf = (float)A.g.L;
     const T zero = A.p.zero;
     for (int s = blockIdx.x * (kThreads / 32) + wid; s < A.n; s += gridDim.x * (kThreads / 32)) {
-        const int a = A.idx ? __ldg(A.idx + s) : s;
-        if (a >= A.n_owned) continue;   // a ghost (uniform across the warp)
+        const int a = storage_of(A, s);
+        if ((unsigned)(a - A.own_lo) >= (unsigned)A.n_owned) continue;   // a ghost (uniform across the warp)
         int ix, iy, iz;
         decode_box(A.bd, __ldg(A.skey + s), ix, iy, iz);
         const float *myp = A.prox.p + 8 * (s >> 1) + (s & 1);
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
                 T gx, gy, gz;
                 int dg;
                 const int t = Q[p];
-                if (pair_force(A, me, ui, A.idx ? __ldg(A.idx + t) : t, gx, gy, gz, dg)) {
+                if (pair_force(A, me, ui, storage_of(A, t), gx, gy, gz, dg)) {
                     fx = fx + gx;
                     fy = fy + gy;
                     fz = fz + gz;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
             for (int p = lane; p < np2; p += 32) {
                 if (p < qn) {
                     const int t = Q[p];
-                    U[p] = A.uid[A.idx ? __ldg(A.idx + t) : t];
+                    U[p] = A.uid[storage_of(A, t)];
                 } else {
                     U[p] = ~0ull;
                     Q[p] = -1;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
                 T gx, gy, gz;
                 int dg = 0;
                 const int t = Q[p];
-                const bool kept = pair_force(A, me, ui, A.idx ? __ldg(A.idx + t) : t, gx, gy, gz, dg);
+                const bool kept = pair_force(A, me, ui, storage_of(A, t), gx, gy, gz, dg);
                 F[p][0] = kept ? gx : zero;
                 F[p][1] = kept ? gy : zero;
                 F[p][2] = kept ? gz : zero;

@@ -7,14 +7,15 @@ every rank derives, bit for bit, from the all-reduced bounding box
 (spatial.py:99-116).  Per step:
 
   1. all-reduce of the 7-double local bbox (min xyz, max xyz, max diameter);
-  2. cg_slab_plan: geometry + owner rank of every owned agent;
-  3. migration: all-to-all of counts, then of packed records (departures
-     leave, arrivals are appended) -- the whole agent row moves;
-  4. halo: the owned agents of the two boundary planes go to rank-1 / rank+1
-     as this step's ghosts (candidates only);
-  5. cg_slab_step: grid rebuild over owned + ghosts on the slab's sub-grid
+  2. cg_slab_plan: geometry, owner rank of every owned agent, and whether it
+     lies in a neighbour's ghost plane (X_q - 1 or X_q+1 of its owner q+-1);
+  3. ONE exchange round: all-to-all of 3 counts per rank pair, then of the
+     packed records -- per destination [migrants][lo ghosts][hi ghosts];
+     migrants leave / join the owned sets (the whole agent row moves),
+     ghosts are this step's candidates only;
+  4. cg_slab_step: grid rebuild over owned + ghosts on the slab's sub-grid
      (planes X_r - 1 .. X_r+1), sweep, gate, cap, apply for owned agents;
-  6. all-reduce of the counters.
+  5. all-reduce of the counters.
 
 An owned agent's candidate set (its 27 global boxes) and its uid-ordered pair
 sum are exactly those of a single-GPU step over the global pool, so
@@ -123,33 +124,17 @@ class SlabRunner:
         ctx, ex, r, W, R = self.ctx, self.ex, self.rank, self.world, self.rec
         bb = ex.allreduce_bbox(ctx.local_bbox())
         counts, planes = ctx.slab_plan(bb, W, r, interaction_radius, box_cap)
-        recv_counts = ex.alltoall_counts(counts)
-        send_counts = counts.copy()
-        send_counts[r] = 0
-        recv_counts[r] = 0
-        nout, nin = int(send_counts.sum()), int(recv_counts.sum())
-        send = ex.buffer(nout * R)
-        if nout:
-            ctx.slab_migrate(ex.ptr(send))
-        recv = ex.alltoall_bytes(send, send_counts * R, recv_counts * R)
-        if nin:
-            ctx.slab_accept(ex.ptr(recv), nin)
-        # halo: boundary planes to the neighbouring slabs
-        hc = ctx.slab_halo_counts()
-        hsend = ex.buffer(int(hc.sum()) * R)
-        if hc.sum():
-            ctx.slab_halo_pack(ex.ptr(hsend))
-        hs = np.zeros(W, np.int64)
-        if r > 0:
-            hs[r - 1] = hc[0]
-        if r < W - 1:
-            hs[r + 1] = hc[1]
-        hr = ex.alltoall_counts(hs)
-        hrecv = ex.alltoall_bytes(hsend, hs * R, hr * R)
-        ng = int(hr.sum())
-        ctx.slab_set_ghosts(ex.ptr(hrecv), ng)
+        recv_counts = ex.alltoall_counts(counts)          # 3 per rank pair
+        send_bytes = counts.reshape(W, 3).sum(1) * R
+        recv_bytes = recv_counts.reshape(W, 3).sum(1) * R
+        send = ex.buffer(int(send_bytes.sum()))
+        ctx.slab_pack(ex.ptr(send))
+        recv = ex.alltoall_bytes(send, send_bytes, recv_bytes)
+        ctx.slab_unpack(ex.ptr(recv), recv_counts)
         st = ctx.slab_step(params5, flags)
         tot = ex.allreduce_sum([st.force_evals, st.candidates, st.degenerate_pairs, st.agent_count])
+        rc = recv_counts.reshape(W, 3)
         return SlabStats(force_evals=int(tot[0]), candidates=int(tot[1]), degenerate_pairs=int(tot[2]),
-                         agents=int(tot[3]), migrated_in=nin, migrated_out=nout, ghosts=ng,
+                         agents=int(tot[3]), migrated_in=int(rc[:, 0].sum()),
+                         migrated_out=int(counts.reshape(W, 3)[:, 0].sum()), ghosts=int(rc[:, 1:].sum()),
                          planes=(int(planes[0]), int(planes[1])))

@@ -3,8 +3,9 @@
 Implements the cg_slab_* contract of include/cellgrid_b200.h with numpy and
 the C oracle, so tests can drive paper_2105_00039_b200.distributed.SlabRunner
 over gloo without a GPU: same record layout (8 pool-dtype scalars + uid),
-same ownership rule (global box plane in [X_r, X_r+1)), same halo planes,
-ghosts as candidates only.
+same ownership rule (global box plane in [X_r, X_r+1)), same ghost planes
+(X_r - 1, X_r+1) and the same one-round exchange layout, ghosts as
+candidates only.
 """
 
 from __future__ import annotations
@@ -56,11 +57,21 @@ class MockSlabContext:
         self.L = L
         self.origin = np.asarray(bb[:3], np.float64) - L
         self.dims = (np.floor((np.asarray(bb[3:6]) - np.asarray(bb[:3])) / L).astype(np.int64) + 3)
-        self.bounds = [(k * int(self.dims[0])) // world for k in range(world + 1)]
+        B = [(k * int(self.dims[0])) // world for k in range(world + 1)]
+        self.bounds = B
         self.rank, self.world = rank, world
-        self.dest = np.searchsorted(self.bounds, self._ix(self.cols["position_x"]), side="right") - 1
-        counts = np.bincount(self.dest, minlength=world).astype(np.int64)
-        return counts, np.array(self.bounds[rank:rank + 2], np.int64)
+        ix = self._ix(self.cols["position_x"])
+        q = np.searchsorted(B, ix, side="right") - 1
+        Bn = np.asarray(B)
+        self.q = q
+        self.up = (q + 1 < world) & (ix == Bn[np.minimum(q + 1, world)] - 1)
+        self.down = (q > 0) & (ix == Bn[q])
+        counts = np.zeros(3 * world, np.int64)
+        for d in range(world):
+            counts[3 * d] = np.count_nonzero(q == d) if d != rank else 0
+            counts[3 * d + 1] = np.count_nonzero(self.up & (q + 1 == d))
+            counts[3 * d + 2] = np.count_nonzero(self.down & (q - 1 == d))
+        return counts, np.array(B[rank:rank + 2], np.int64)
 
     def _records(self, idx):
         rec = np.empty(idx.shape[0], self.rec_dtype)
@@ -74,38 +85,29 @@ class MockSlabContext:
     def _read(self, ptr, count):
         return _view(ptr, count * self.record_bytes).view(self.rec_dtype).copy()
 
-    def slab_migrate(self, ptr):
-        leave = np.nonzero(self.dest != self.rank)[0]
-        leave = leave[np.argsort(self.dest[leave], kind="stable")]
-        self._write(ptr, self._records(leave))
-        keep = self.dest == self.rank
+    def slab_pack(self, ptr):
+        q, r = self.q, self.rank
+        runs = []
+        for d in range(self.world):
+            runs.append(np.nonzero((q == d) & (d != r))[0])
+            runs.append(np.nonzero(self.up & (q + 1 == d))[0])
+            runs.append(np.nonzero(self.down & (q - 1 == d))[0])
+        self._write(ptr, self._records(np.concatenate(runs)))
+        keep = q == r
         for c in COLS:
             self.cols[c] = self.cols[c][keep]
         self.uid = self.uid[keep]
 
-    def slab_accept(self, ptr, count):
-        rec = self._read(ptr, count)
+    def slab_unpack(self, ptr, recv_counts):
+        rc = np.asarray(recv_counts, np.int64).reshape(self.world, 3)
+        rec = self._read(ptr, int(rc.sum()))
+        starts = np.concatenate([[0], np.cumsum(rc.ravel())])
+        seg = [rec[starts[k]:starts[k + 1]] for k in range(3 * self.world)]
+        mig = np.concatenate(seg[0::3])
         for k, c in enumerate(COLS):
-            self.cols[c] = np.concatenate([self.cols[c], rec["v"][:, k]])
-        self.uid = np.concatenate([self.uid, rec["uid"]])
-
-    def _halo_lists(self):
-        ix = self._ix(self.cols["position_x"])
-        lo = np.nonzero(ix == self.bounds[self.rank])[0] if self.rank > 0 else np.zeros(0, np.int64)
-        hi = (np.nonzero(ix == self.bounds[self.rank + 1] - 1)[0] if self.rank < self.world - 1
-              else np.zeros(0, np.int64))
-        return lo, hi
-
-    def slab_halo_counts(self):
-        lo, hi = self._halo_lists()
-        return np.array([lo.shape[0], hi.shape[0]], np.int64)
-
-    def slab_halo_pack(self, ptr):
-        lo, hi = self._halo_lists()
-        self._write(ptr, self._records(np.concatenate([lo, hi])))
-
-    def slab_set_ghosts(self, ptr, count):
-        self.ghosts = self._read(ptr, count)
+            self.cols[c] = np.concatenate([self.cols[c], mig["v"][:, k]])
+        self.uid = np.concatenate([self.uid, mig["uid"]])
+        self.ghosts = np.concatenate(seg[1::3] + seg[2::3])
 
     def slab_step(self, params5, flags=0):
         from paper_2105_00039_b200.pool import AgentPool

@@ -1,4 +1,4 @@
-"""x-slab decomposition host logic on CPU: world-size 2 over gloo, each rank a
+"""x-slab decomposition host logic on CPU: world-size 2 and 3 over gloo, each rank a
 numpy/oracle mock of the slab C ABI (tests/slab_mock.py), driven by the real
 SlabRunner.  The union of the ranks' pools after several steps (with agents
 crossing slab boundaries) must equal a single-process oracle run bit for bit,
@@ -44,7 +44,7 @@ def _worker(rank, world, port, steps, params5, out_q):
     full = _pool(1.0, True)
     # initial distribution ignores the slab rule (uid parity): the first step
     # migrates about half of each rank's agents
-    mine = (full.uid % 2) == rank
+    mine = (full.uid % world) == rank
     from paper_2105_00039_b200.pool import AgentPool
     sub = AgentPool(position_x=full.position_x[mine], position_y=full.position_y[mine],
                     position_z=full.position_z[mine], diameter=full.diameter[mine],
@@ -58,8 +58,9 @@ def _worker(rank, world, port, steps, params5, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("params5", [PARAMS5, np.array([2.0, 1.0, 2.0, 3.0, 0.1])])
-def test_slab_two_ranks_match_single_process(params5):
+@pytest.mark.parametrize("world,params5", [(2, PARAMS5), (2, np.array([2.0, 1.0, 2.0, 3.0, 0.1])),
+                                           (3, PARAMS5)])
+def test_slab_ranks_match_single_process(world, params5):
     import multiprocessing as mp
     import oracle
     from paper_2105_00039_b200.mechanics import ForceParams
@@ -67,7 +68,7 @@ def test_slab_two_ranks_match_single_process(params5):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, steps, params5, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, steps, params5, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=240) for _ in procs], key=lambda t: t[0])
@@ -93,6 +94,6 @@ def test_slab_two_ranks_match_single_process(params5):
         assert np.array_equal(mine, getattr(ref, col)[order_ref]), col
     # global counters of every step agree on both ranks and with the oracle
     for k in range(steps):
-        assert res[0][3][k][:2] == res[1][3][k][:2] == ref_counters[k]
+        assert all(r[3][k][:2] == ref_counters[k] for r in res)
     # agents did cross slab boundaries
-    assert sum(x[2] for x in res[0][3]) + sum(x[2] for x in res[1][3]) > 0
+    assert sum(x[2] for r in res for x in r[3]) > 0
