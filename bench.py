@@ -147,12 +147,13 @@ def measured_hbm_peak():
         return 6650.0, "fallback"
 
 
-def profiled_traffic(config, precision):
-    """Per-launch DRAM bytes of the sweep from the committed ncu capture, if any."""
+def profiled_traffic(config, precision, kernel):
+    """Per-launch DRAM bytes (read + write) of ``kernel`` from the committed
+    ncu --set full capture (profiles/traffic.json), if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get("%s_%s" % (config, precision))
-    except (OSError, ValueError):
+            return json.load(fh).get("%s_%s" % (config, precision), {}).get(kernel)
+    except (OSError, ValueError, AttributeError):
         return None
 
 
@@ -388,7 +389,17 @@ def main():
     ms = ev0.elapsed_time(ev1) / args.steps
     ms = reduce_max(ms, world)
     stats = [ctx.fetch_stats(i) for i in ids[-min(len(ids), 60):]]
-    t_force = float(np.mean([s.t_force_ms for s in stats]))
+    # the dominant sweep kernel of the timed region (most total time): the
+    # grid sweep (kind 0), the grid sweep that also builds neighbour lists
+    # (kind 1) or the list sweep (kind 2, csrc/list.cuh)
+    kinds = {}
+    for s_ in stats:
+        kinds.setdefault(int(s_.sweep_kind), []).append(float(s_.t_force_ms))
+    dom = max(kinds, key=lambda k: sum(kinds[k]))
+    t_force = float(np.mean(kinds[dom]))
+    kernel_name = {0: "sweep7_kernel", 1: "sweep7_kernel_list_build", 2: "list_sweep_kernel"}[dom]
+    sweep_mix = {{0: "grid_sweep", 1: "grid_sweep_list_build", 2: "list_sweep"}[k]:
+                 {"steps": len(v), "mean_ms": float(np.mean(v))} for k, v in sorted(kinds.items())}
     evals = float(np.mean([s.force_evals for s in stats]))
     cands = float(np.mean([s.candidates for s in stats]))
     value = n * world / (ms * 1e-3)
@@ -442,9 +453,9 @@ def main():
                    "l2": "inputs larger than L2 (%.0f MB of agent state per GPU)" % (n * (6 * np.dtype(pool.dtype).itemsize + 8) / 1e6),
                    "parallelism": "single GPU" if world == 1 else "replicas x%d (no halo exchange)" % world},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.precision),
-                     "kernel": "sweep7_kernel", "alg_bytes_per_agent": bal,
-                     "kernel_ms": t_force, "peak_source": peak_src},
+                     "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.precision, kernel_name),
+                     "kernel": kernel_name, "alg_bytes_per_agent": bal,
+                     "kernel_ms": t_force, "peak_source": peak_src, "sweep_mix": sweep_mix},
         "step_roofline_frac": n * bal / (ms * 1e-3) / 1e9 / peak,
         "pair_interactions_per_s": evals * world / (ms * 1e-3),
         "candidates_per_s": cands * world / (ms * 1e-3),

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CG_ABI_VERSION 4
+#define CG_ABI_VERSION 5
 
 /* status codes */
 #define CG_OK 0
@@ -56,6 +56,9 @@ extern "C" {
 #define CG_OPT_RELAYOUT_EVERY 4 /* move the records into slot order on every k-th sort step (k >= 1, default 1) */
 #define CG_OPT_PATH 5           /* 0 = auto (by agents per box), 1 = sparse (uid-sorted survivor lists),
                                    2 = dense (boxes ordered by (z, uid), CG_OPT_SUMMATION applies) */
+#define CG_OPT_LIST_SKIN 6      /* neighbour-list reuse on the sparse path: -1 = auto (skin 0.1 x box
+                                   length, default), 0 = off, k > 0 = skin of k/1000 length units.
+                                   Results are identical with or without it (csrc/list.cuh). */
 
 typedef struct cg_context cg_context;
 
@@ -72,6 +75,8 @@ typedef struct {
     double box_length;
     double origin[3];
     float t_sort_ms, t_grid_ms, t_force_ms, t_total_ms;   /* CUDA-event times */
+    int32_t sweep_kind;         /* 0 grid sweep, 1 grid sweep + neighbour-list build, 2 list sweep */
+    int32_t reserved;
 } cg_step_stats;
 
 int cg_abi_version(void);
@@ -129,6 +134,11 @@ int cg_force_phase(cg_context *ctx, int64_t n, const void *px, const void *py, c
                    const int64_t *box_index, int64_t dimx, int64_t dimy, int64_t dimz,
                    const void *params7, void *out_dx, void *out_dy, void *out_dz,
                    int64_t counters[3]);
+
+/* Neighbour-list reuse counters (CG_OPT_LIST_SKIN): out[0] list builds,
+ * out[1] steps served from lists, out[2] lists currently valid, out[3] skin of
+ * the last build in 1e-6 length units. */
+int cg_list_stats(cg_context *ctx, int64_t out[4]);
 
 /* ---- radius queries: kernels.grid_neighbor_counts /
  * grid_neighbor_fill (kernels.py:427-520) behind spatial.neighbor_counts /

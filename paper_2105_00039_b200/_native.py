@@ -21,7 +21,7 @@ CG_OK, CG_ERR_VALUE, CG_ERR_GRID_OVERFLOW, CG_ERR_STENCIL = 0, 1, 2, 3
 CG_ERR_POOL_CAPACITY, CG_ERR_CUDA, CG_ERR_NO_DEVICE, CG_ERR_STATE = 4, 5, 6, 7
 CG_FP64, CG_FP32 = 0, 1
 CG_STEP_SORT, CG_STEP_FREEZE, CG_STEP_RECORD = 1, 2, 4
-CG_OPT_SUMMATION, CG_OPT_SWEEP, CG_OPT_RELAYOUT_EVERY, CG_OPT_PATH = 1, 3, 4, 5
+CG_OPT_SUMMATION, CG_OPT_SWEEP, CG_OPT_RELAYOUT_EVERY, CG_OPT_PATH, CG_OPT_LIST_SKIN = 1, 3, 4, 5, 6
 
 # every symbol include/cellgrid_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_last_error",
@@ -30,7 +30,8 @@ EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_
             "cg_record_export", "cg_box_ids", "cg_force_phase", "cg_launch_count",
             "cg_host_alloc", "cg_host_free", "cg_record_bytes", "cg_reserve", "cg_local_bbox",
             "cg_slab_plan", "cg_slab_pack", "cg_slab_unpack",
-            "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill")
+            "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill",
+            "cg_list_stats")
 
 
 class GridOverflowError(RuntimeError):
@@ -56,7 +57,8 @@ class StepStatsC(ctypes.Structure):
                 ("grid_occupied_boxes", ctypes.c_int64), ("grid_max_occupancy", ctypes.c_int64),
                 ("box_length", ctypes.c_double), ("origin", ctypes.c_double * 3),
                 ("t_sort_ms", ctypes.c_float), ("t_grid_ms", ctypes.c_float),
-                ("t_force_ms", ctypes.c_float), ("t_total_ms", ctypes.c_float)]
+                ("t_force_ms", ctypes.c_float), ("t_total_ms", ctypes.c_float),
+                ("sweep_kind", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _lib = None
@@ -97,6 +99,7 @@ def load():
                        ctypes.c_int),
         "cg_force_phase": ([_P, _I64] + [_P] * 7 + [_I64] * 3 + [_P] * 5, ctypes.c_int),
         "cg_neighbor_counts": ([_P, ctypes.c_double, _P], ctypes.c_int),
+        "cg_list_stats": ([_P, _P], ctypes.c_int),
         "cg_neighbor_fill": ([_P, ctypes.c_double, _P, _P], ctypes.c_int),
         "cg_record_bytes": ([_P], _I64),
         "cg_reserve": ([_P, _I64], ctypes.c_int),
@@ -111,7 +114,7 @@ def load():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
-    if L.cg_abi_version() != 4:
+    if L.cg_abi_version() != 5:
         raise NativeUnavailable("ABI version mismatch")
     _lib = L
     return L
@@ -226,6 +229,13 @@ class Context:
         bc = np.empty(num_boxes, np.int64)
         check(load().cg_grid_export(self.h, ptr(bi), ptr(bc)), self.h)
         return bi, bc
+
+    def list_stats(self):
+        """(builds, list steps, valid, skin) of the neighbour-list reuse."""
+        out = np.zeros(4, np.int64)
+        check(load().cg_list_stats(self.h, ptr(out)), self.h)
+        return {"builds": int(out[0]), "list_steps": int(out[1]), "valid": bool(out[2]),
+                "skin": out[3] * 1e-6}
 
     # ---- radius queries (spatial.neighbor_counts / neighbor_csr)
     def neighbor_counts(self, radius):

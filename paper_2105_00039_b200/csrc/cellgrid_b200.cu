@@ -42,6 +42,7 @@
 #include "slab.cuh"
 #include "sweep_warp.cuh"
 #include "query.cuh"
+#include "list.cuh"
 
 using namespace cg;
 
@@ -112,6 +113,17 @@ struct cg_context {
     bool last_record = false;
     bool last_dense = false;
     bool grid_current = false;    // the grid indexes the stored positions (cg_build_grid)
+    // neighbour-list reuse (list.cuh): skin < 0 = auto (0.1 x box length), 0 = off
+    double list_skin = -1.0;
+    int *nbr = nullptr, *nbr_n = nullptr;
+    int64_t nbr_cap = 0;
+    bool list_valid = false;      // lists cover every pair that can overlap now
+    int last_kind = 0;            // previous step: 0 other, 1 list build, 2 list step
+    bool last_freeze = false;
+    double list_D = 0.0;          // bound on any agent's motion since the build
+    double list_skin_used = 0.0;
+    int list_life = 0, list_backoff = 0, list_wait = 0;
+    int64_t list_builds = 0, list_steps = 0;
     int rot = 0;                  // relaid slab sub-grid: slot s lives at storage s - rot (lo ghosts in
                                   // the buffers' front headroom, owned agents at [0, n_owned))
     int64_t sort_steps = 0;
@@ -177,6 +189,12 @@ static void free_agents(cg_context *c)
         if (p) cudaFree(p);
     c->b = Buffers{};
     c->cap = 0;
+    if (c->nbr) cudaFree(c->nbr);
+    if (c->nbr_n) cudaFree(c->nbr_n);
+    c->nbr = c->nbr_n = nullptr;
+    c->nbr_cap = 0;
+    c->list_valid = false;
+    c->last_kind = 0;
 }
 
 static int alloc_agents(cg_context *c, int64_t cap)
@@ -333,7 +351,7 @@ static int standalone_bbox(cg_context *c)
     finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, nullptr, c->bbox_dev, FINISH_BBOX);
     LAUNCH_CHECK(c);
     c->launches += 2;
-    CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));
     c->bbox_valid = true;
     return CG_OK;
@@ -511,6 +529,15 @@ static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
 template <typename T>
 static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
 {
+    if (!c->last_dense && A.nbr) {   // sparse sweep that also builds the neighbour lists
+        cudaStream_t st = c->stream;
+        CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
+        sweep7_kernel<T, true, false, 16, false, CG_SPARSE_MINB, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
+        sweep7_overflow<T, true, false, 16, true><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
+        LAUNCH_CHECK(c);
+        c->launches += 2;
+        return CG_OK;
+    }
     if (!c->last_dense) {
         // sparse: survivors summed in uid order (deterministic and bit-identical to
         // the reference whatever the slot order in a box); agents with more than
@@ -548,8 +575,22 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
     return CG_OK;
 }
 
+// bbox shell (see sweep7.cuh): an agent can only become extreme if it ends
+// within max_displacement (+ rounding slack) of the old bbox faces
+static void bbox_shell(const cg_context *c, double md, double shell_lo[3], double shell_hi[3])
+{
+    const bool ok = std::isfinite(md) && md >= 0.0;
+    for (int q = 0; q < 3; ++q) {
+        const double lo = c->bbox_host[q], hi = c->bbox_host[3 + q];
+        const double slack = 1e-6 * (std::fabs(lo) + std::fabs(hi) + 1.0);
+        const double B = ok ? md * (1.0 + 1e-6) + slack : INFINITY;
+        shell_lo[q] = lo + B;
+        shell_hi[q] = hi - B;
+    }
+}
+
 template <typename T>
-static int run_sweep(cg_context *c, const double params[5], bool freeze, bool record)
+static int run_sweep(cg_context *c, const double params[5], bool freeze, bool record, bool build_lists = false)
 {
     const int n = (int)c->n;
     cudaStream_t st = c->stream;
@@ -621,21 +662,18 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     A.slots = c->slots;
     // bbox shell (see sweep7.cuh): an agent can only become extreme if it ends
     // within max_displacement (+ rounding slack) of the old bbox faces
-    {
-        const double md = (double)P.max_disp;
-        const bool ok = std::isfinite(md) && md >= 0.0;
-        for (int q = 0; q < 3; ++q) {
-            const double lo = c->bbox_host[q], hi = c->bbox_host[3 + q];
-            const double slack = 1e-6 * (std::fabs(lo) + std::fabs(hi) + 1.0);
-            const double B = ok ? md * (1.0 + 1e-6) + slack : INFINITY;
-            A.shell_lo[q] = lo + B;
-            A.shell_hi[q] = hi - B;
-        }
-    }
+    bbox_shell(c, (double)P.max_disp, A.shell_lo, A.shell_hi);
     A.ovf = c->b.ovf;
     A.ovf_count = c->ovf_count;
     A.n_owned = (int)c->n_owned;
     A.own_lo = c->rot;
+    if (build_lists && !c->last_dense) {
+        A.nbr = c->nbr;
+        A.nbr_n = c->nbr_n;
+        A.nbr_stride = c->nbr_cap;
+        A.skin = (T)c->list_skin_used;
+        A.skin_f = nextafterf((float)c->list_skin_used, INFINITY);
+    }
     int rc = launch_sweep7<T>(c, A);
     if (rc) return rc;
     unsigned long long *stat = c->stat_dev + (c->steps_done % kRing) * kStatSlots;
@@ -645,8 +683,106 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     LAUNCH_CHECK(c);
     c->launches += 1;
     if (!freeze)
-        CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
     c->bbox_valid = true;
+    return CG_OK;
+}
+
+// ---------------------------------------------------------------- neighbour-list reuse
+static int ensure_lists(cg_context *c)
+{
+    if (c->nbr && c->nbr_cap == c->cap) return CG_OK;
+    if (c->nbr) cudaFree(c->nbr);
+    if (c->nbr_n) cudaFree(c->nbr_n);
+    c->nbr = c->nbr_n = nullptr;
+    c->nbr_cap = 0;
+    CUDA_TRY(c, cudaMalloc(&c->nbr, sizeof(int) * (size_t)kListCap * (size_t)c->cap));
+    CUDA_TRY(c, cudaMalloc(&c->nbr_n, sizeof(int) * (size_t)c->cap));
+    c->nbr_cap = c->cap;
+    return CG_OK;
+}
+
+// After the previous step's readback: lists built last step become valid if
+// no agent overflowed; every step on valid lists adds its largest
+// displacement (+ rounding of the position update) to the motion bound D.
+template <typename T>
+static void list_account(cg_context *c)
+{
+    if (c->last_kind == 1) {
+        c->list_valid = c->bbox_host[8] == 0.0;
+        c->list_D = 0.0;
+        c->list_life = 0;
+        if (!c->list_valid) {   // some agent has more than kListCap partners: back off
+            c->list_backoff = c->list_backoff ? std::min(2 * c->list_backoff, 64) : 4;
+            c->list_wait = c->list_backoff;
+        }
+    }
+    if (c->list_valid && c->last_kind != 0 && !c->last_freeze) {
+        double M = 0.0;
+        for (int q = 0; q < 6; ++q) M = std::max(M, std::fabs(c->bbox_host[q]));
+        const double ulp = M * (sizeof(T) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07);
+        c->list_D += std::sqrt(std::max(c->bbox_host[7], 0.0)) * (1.0 + 1e-6) + 2.0 * ulp;
+    }
+}
+
+template <typename T>
+static int list_step_t(cg_context *c, const Geometry &g, const double params[5], bool sort, bool freeze,
+                       bool record)
+{
+    const int n = (int)c->n;
+    cudaStream_t st = c->stream;
+    const int slot = (int)(c->steps_done % kRing);
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][0], st));
+    int rc;
+    if ((rc = ensure_boxes(c, g.nb))) return rc;
+    c->geo = g;
+    c->bd = make_decode(g);
+    unsigned long long *stat = c->stat_dev + slot * kStatSlots;
+    CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
+    const int cp = c->cur_pos, ca = c->cur_attr;
+    box_keys<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, g, 1.0 / g.L, (const Rec<T> *)c->b.rec[cp], c->count,
+                                                        c->b.key_rank);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
+    ListArgs<T> A{};
+    A.n = n;
+    A.g = g;
+    A.bd = c->bd;
+    A.key_rank = c->b.key_rank;
+    A.off = c->offset;
+    A.rec = (const Rec<T> *)c->b.rec[cp];
+    A.adh = (const T *)c->b.adh[ca];
+    A.uid = c->b.uid[ca];
+    A.p = make_params<T>(params);
+    A.nbr = c->nbr;
+    A.nbr_n = c->nbr_n;
+    A.nbr_stride = c->nbr_cap;
+    A.disp_x = (T *)c->b.disp[0];
+    A.disp_y = (T *)c->b.disp[1];
+    A.disp_z = (T *)c->b.disp[2];
+    A.new_rec = freeze ? nullptr : (Rec<T> *)c->b.rec[1 - cp];
+    A.rec_m = record ? c->b.rec_m : nullptr;
+    A.rec_nk = record ? c->b.rec_nk : nullptr;
+    A.pkey = sort ? c->b.pkey[ca] : nullptr;
+    A.slots = c->slots;
+    bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
+    list_sweep_kernel<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);
+    finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, stat, c->bbox_dev,
+                                         FINISH_COUNTERS | (freeze ? 0 : FINISH_BBOX));
+    LAUNCH_CHECK(c);
+    c->launches += 2;
+    if (!freeze)
+        CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    c->bbox_valid = true;
+    c->have_grid = true;
+    c->relaid = false;      // slot arrays are not rebuilt: exports use key_rank
+    c->last_dense = false;
+    if (sort) c->geo_sort = g;
+    c->list_life++;
+    c->list_steps++;
     return CG_OK;
 }
 
@@ -677,17 +813,66 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
     double origin[3];
     int64_t dims64[3];
     int rc;
-    // build_grid records event 0 after the bbox readback + host geometry, so
-    // the per-phase times are device times
-    if ((rc = build_grid<T>(c, ir, box_cap, relayout, sort, origin, dims64))) return rc;
-    CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
-    if (sort) {
-        c->sort_steps++;
-        c->pres_state = PRES_PENDING;   // the reference re-sorted its pool this step
-    } else if (relayout) {
-        c->pres_state = PRES_PENDING;
+    // the previous step's readback (bbox, largest displacement, list
+    // overflows), then the geometry; event 0 is recorded after it, so the
+    // per-phase times are device times
+    if (!c->bbox_valid) {
+        c->list_valid = false;
+        c->last_kind = 0;
+        if ((rc = standalone_bbox<T>(c))) return rc;
+    } else {
+        CUDA_TRY(c, cudaStreamSynchronize(st));
     }
-    if ((rc = run_sweep<T>(c, params, freeze, record))) return rc;
+    list_account<T>(c);
+    Geometry g;
+    if ((rc = host_geometry(c, c->bbox_host, ir, box_cap, g, dims64, origin))) return rc;
+    const bool lists_on = c->list_skin != 0.0 && c->sweep_impl == 1 && c->n > 1;
+    bool use_list = false;
+    if (lists_on && c->list_valid) {
+        if (2.0 * c->list_D <= 0.999 * c->list_skin_used && c->nbr_cap == c->cap) {
+            use_list = true;
+        } else {   // expired: a list that served fewer than 2 steps makes the next builds wait
+            c->list_valid = false;
+            if (c->list_life < 2) {
+                c->list_backoff = c->list_backoff ? std::min(2 * c->list_backoff, 64) : 4;
+                c->list_wait = c->list_backoff;
+            } else {
+                c->list_backoff = 0;
+            }
+        }
+    }
+    if (use_list) {
+        if ((rc = list_step_t<T>(c, g, params, sort, freeze, record))) return rc;
+        if (sort) {
+            c->sort_steps++;
+            c->pres_state = PRES_PENDING;
+        }
+        c->last_kind = 2;
+        S.sweep_kind = 2;
+    } else {
+        bool build = lists_on && c->list_wait == 0;
+        if (c->list_wait > 0) c->list_wait--;
+        if (build) {
+            if ((rc = ensure_lists(c))) return rc;
+            c->list_skin_used = c->list_skin < 0 ? 0.1 * g.L : c->list_skin;
+            build = c->list_skin_used > 0 && c->list_skin_used <= g.L;
+        }
+        if ((rc = build_grid_geo<T>(c, g, relayout, sort))) return rc;
+        CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
+        if (sort) {
+            c->sort_steps++;
+            c->pres_state = PRES_PENDING;   // the reference re-sorted its pool this step
+        } else if (relayout) {
+            c->pres_state = PRES_PENDING;
+        }
+        build = build && !c->last_dense;
+        c->list_valid = false;
+        if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
+        c->last_kind = build ? 1 : 0;
+        S.sweep_kind = build ? 1 : 0;
+        if (build) c->list_builds++;
+    }
+    c->last_freeze = freeze;
     if (!freeze) c->cur_pos = 1 - c->cur_pos;
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][3], st));
     CUDA_TRY(c, cudaMemcpyAsync(c->stat_host + slot * kStatSlots, c->stat_dev + slot * kStatSlots,
@@ -920,6 +1105,8 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
 {
     auto &S = c->slab;
     if (!S.planned || !S.packed) return fail(c, CG_ERR_STATE, "cg_slab_step without cg_slab_plan / cg_slab_pack");
+    c->list_valid = false;
+    c->last_kind = 0;
     const int slot = (int)(c->steps_done % kRing);
     cg_step_stats &St = c->ring[slot];
     std::memset(&St, 0, sizeof St);
@@ -1014,8 +1201,8 @@ int cg_create(int device, int precision, cg_context **out)
     chk(cudaMalloc(&c->maxd_enc, sizeof(unsigned long long)));
     chk(cudaMalloc(&c->ovf_count, sizeof(unsigned)));
     chk(cudaMalloc(&c->block_counters, sizeof(unsigned long long) * 3 * kMaxCounterBlocks));
-    chk(cudaMalloc(&c->bbox_dev, sizeof(double) * 8));
-    chk(cudaMallocHost(&c->bbox_host, sizeof(double) * 8));
+    chk(cudaMalloc(&c->bbox_dev, sizeof(double) * 16));
+    chk(cudaMallocHost(&c->bbox_host, sizeof(double) * 16));
     chk(cudaMalloc(&c->stat_dev, sizeof(unsigned long long) * kStatSlots * kRing));
     chk(cudaMallocHost(&c->stat_host, sizeof(unsigned long long) * kStatSlots * kRing));
     for (int r = 0; r < kRing; ++r)
@@ -1093,6 +1280,12 @@ int cg_set_option(cg_context *c, int key, int value)
         c->path = value;
         return CG_OK;
     }
+    if (key == CG_OPT_LIST_SKIN && value >= -1) {
+        c->list_skin = value < 0 ? -1.0 : value * 1e-3;
+        c->list_valid = false;
+        c->last_kind = 0;
+        return CG_OK;
+    }
     return fail(c, CG_ERR_VALUE, "bad option %d=%d", key, value);
 }
 
@@ -1110,6 +1303,12 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
     }
     c->n = n;
     c->n_owned = n;
+    c->list_valid = false;
+    c->last_kind = 0;
+    // lists pay off only over consecutive resident steps: none on the first
+    // step after an upload (a caller that uploads before every step, like
+    // engine.step, never pays for a build)
+    c->list_wait = std::max(c->list_wait, 1);
     c->grid_current = false;
     c->slab.planned = false;
     c->cur_pos = c->cur_attr = 0;
@@ -1543,6 +1742,16 @@ static int neighbor_check(cg_context *c, double radius)
 }
 
 extern "C" {
+
+int cg_list_stats(cg_context *c, int64_t out[4])
+{
+    if (!c || !out) return CG_ERR_VALUE;
+    out[0] = c->list_builds;
+    out[1] = c->list_steps;
+    out[2] = c->list_valid ? 1 : 0;
+    out[3] = (int64_t)llround(c->list_skin_used * 1e6);
+    return CG_OK;
+}
 
 int cg_neighbor_counts(cg_context *c, double radius, int64_t *counts)
 {

@@ -24,9 +24,21 @@ namespace cg {
 // Per-step reduction slots: blocks spread their atomics over kSlots slots
 // (blockIdx % kSlots) so no address sees more than a few hundred updates.
 // slot layout: [0..2] min x,y,z (ordered u64), [3..5] max x,y,z, [6] evals,
-// [7] candidates, [8] degenerate pairs.
+// [7] candidates, [8] degenerate pairs, [9] max squared displacement
+// (ordered u64), [10] neighbour-list overflows.
 constexpr int kSlots = 512;
-constexpr int kSlotWords = 9;
+constexpr int kSlotWords = 11;
+
+// reduction of slot word k: 0 = min, 1 = max, 2 = sum
+__device__ __forceinline__ int slot_op(int k)
+{
+    return k < 3 ? 0 : (k < 6 || k == 9) ? 1 : 2;
+}
+__device__ __forceinline__ unsigned long long slot_combine(int k, unsigned long long a, unsigned long long b)
+{
+    const int op = slot_op(k);
+    return op == 0 ? min(a, b) : op == 1 ? max(a, b) : a + b;
+}
 
 __device__ __forceinline__ double warp_min(double v)
 {
@@ -134,7 +146,7 @@ __global__ void finish_step(unsigned long long *__restrict__ slots, double max_d
 #pragma unroll
         for (int k = 0; k < kSlotWords; ++k) {
             const unsigned long long u = slots[s * kSlotWords + k];
-            v[k] = k < 3 ? min(v[k], u) : (k < 6 ? max(v[k], u) : v[k] + u);
+            v[k] = slot_combine(k, v[k], u);
             slots[s * kSlotWords + k] = slot_init(k);
         }
     }
@@ -145,7 +157,7 @@ __global__ void finish_step(unsigned long long *__restrict__ slots, double max_d
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long u = __shfl_xor_sync(0xffffffffu, t, o);
-            t = k < 3 ? min(t, u) : (k < 6 ? max(t, u) : t + u);
+            t = slot_combine(k, t, u);
         }
         if (lane == 0) red[k][w] = t;
     }
@@ -154,11 +166,16 @@ __global__ void finish_step(unsigned long long *__restrict__ slots, double max_d
         const int k = threadIdx.x;
         unsigned long long t = red[k][0];
         for (int q = 1; q < kThreads / 32; ++q)
-            t = k < 3 ? min(t, red[k][q]) : (k < 6 ? max(t, red[k][q]) : t + red[k][q]);
+            t = slot_combine(k, t, red[k][q]);
         if (k < 6) {
             if (what & FINISH_BBOX) bbox_out[k] = dec_ordered(t);
-        } else if (what & FINISH_COUNTERS) {
-            stat[2 + (k - 6)] = t;
+        } else if (k < 9) {
+            if (what & FINISH_COUNTERS) stat[2 + (k - 6)] = t;
+        } else if (k == 9) {
+            bbox_out[7] = t ? dec_ordered(t) : 0.0;   // max squared displacement of the step
+        } else {
+            if (what & FINISH_COUNTERS) stat[5] = t;  // neighbour-list overflows
+            bbox_out[8] = (double)t;
         }
         if (k == 0 && (what & FINISH_BBOX)) bbox_out[6] = max_diameter;
     }

@@ -1,0 +1,180 @@
+// list.cuh -- neighbour-list reuse between grid sweeps.
+//
+// The reference's force phase (kernels.py:148-277) keeps, for agent i, the
+// stencil candidates j with delta = (ri + rj) - dist > 0 and sums their pair
+// forces in ascending uid.  The result depends only on that SET of pairs (every
+// overlapping pair lies inside the 27-box stencil, L >= ri + rj), so it may be
+// enumerated from any superset.  A build sweep (sweep7 with LIST) records, per
+// agent and in uid order, every partner within ri + rj + skin; while the
+// agents have moved by at most D in total since the build, with 2 D <= skin,
+// every pair that overlaps now is in those lists (triangle inequality).  The
+// list sweep then runs the reference's exact pair expressions over the list --
+// bit-identical displacements, positions and counters -- without the stencil
+// walk.  The per-step grid (box ids, counts, offsets, occupancy stats, the
+// presentation key) is still rebuilt every step: m (the candidates counter)
+// and the statistics are the reference's, from this step's grid.
+#pragma once
+
+#include "common.cuh"
+#include "grid.cuh"
+#include "sweep7.cuh"
+
+namespace cg {
+
+template <typename T>
+struct ListArgs {
+    int n;
+    Geometry g;
+    BoxDecode bd;
+    const int2 *key_rank;     // this step's box of every storage index
+    const int *off;           // this step's CSR offsets
+    const Rec<T> *rec;
+    const T *adh;
+    const uint64_t *uid;
+    Params<T> p;
+    const int *nbr;           // [kListCap][nbr_stride]
+    const int *nbr_n;
+    long long nbr_stride;
+    T *disp_x, *disp_y, *disp_z;
+    Rec<T> *new_rec;          // nullptr when frozen
+    int *rec_m, *rec_nk;      // nullptr unless recording
+    int *pkey;                // this step's box (sort steps), nullptr otherwise
+    unsigned long long *slots;
+    double shell_lo[3], shell_hi[3];
+};
+
+// coincident centres (kernels.py:244-257): out of line, it is rare and its
+// transcendental code would otherwise hold registers in the pair loop
+template <typename T>
+__device__ __noinline__ void degenerate_pair(uint64_t ui, uint64_t uj, T mag, T &fx, T &fy, T &fz)
+{
+    double ux, uy, uz;
+    degenerate_dir(ui < uj ? ui : uj, ui < uj ? uj : ui, ux, uy, uz);
+    const double sign = ui < uj ? 1.0 : -1.0;
+    fx = fx + (T)((double)mag * (sign * ux));
+    fy = fy + (T)((double)mag * (sign * uy));
+    fz = fz + (T)((double)mag * (sign * uz));
+}
+
+#ifndef CG_LIST_MINB
+#define CG_LIST_MINB 4
+#endif
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, CG_LIST_MINB) list_sweep_kernel(ListArgs<T> A)
+{
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned c_m = 0, c_nk = 0, c_nd = 0;
+    float dmax2 = 0.f;
+    if (a < A.n) {
+        const int key = A.key_rank[a].x;
+        if (A.pkey) A.pkey[a] = key;
+        int ix, iy, iz;
+        decode_box(A.bd, key, ix, iy, iz);
+        // m: agents of the 27 clamped boxes minus self (_gather_stencil)
+        int m = -1;
+        {
+            const int z0 = max(iz - 1, 0), z1 = min(iz + 1, A.g.dimz - 1);
+#pragma unroll
+            for (int ox = -1; ox <= 1; ++ox) {
+                const int nx = ix + ox;
+                if ((unsigned)nx >= (unsigned)A.g.dimx) continue;
+#pragma unroll
+                for (int oy = -1; oy <= 1; ++oy) {
+                    const int ny = iy + oy;
+                    if ((unsigned)ny >= (unsigned)A.g.dimy) continue;
+                    const int base = (nx * A.g.dimy + ny) * A.g.dimz;
+                    m += __ldg(A.off + base + z1 + 1) - __ldg(A.off + base + z0);
+                }
+            }
+        }
+        const T half = T(0.5), zero = A.p.zero;
+        const Rec<T> me = A.rec[a];
+        const T xi = me.x, yi = me.y, zi = me.z;
+        const T ri = me.d * half;
+        T fx = zero, fy = zero, fz = zero;
+        int nk = 0, nd = 0;
+        T last_rj = T(-1), last_req = zero;
+        const int cnt = A.nbr_n[a];
+        const int *L = A.nbr + a;
+        // two indices and one record ahead of the pair being evaluated
+        int jn = cnt > 0 ? __ldg(L) : 0;
+        int jnn = cnt > 1 ? __ldg(L + A.nbr_stride) : 0;
+        Rec<T> o;
+        if (cnt > 0) o = A.rec[jn];
+#pragma unroll 1
+        for (int p = 0; p < cnt; ++p) {
+            const int jc = jn;
+            const Rec<T> co = o;
+            jn = jnn;
+            if (p + 1 < cnt) o = A.rec[jn];
+            if (p + 2 < cnt) jnn = __ldg(L + (p + 2) * A.nbr_stride);
+            // the reference's pass-1 test and pass-2 expressions (kernels.py:198-257)
+            const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;
+            const T rj = co.d * half;
+            const T s2 = dx * dx + dy * dy + dz * dz;
+            const T rsum = ri + rj;
+            // s2 > rsum^2 (1 + 2^-40) implies fl(sqrt(s2)) > rsum: not overlapping, no sqrt needed
+            if (s2 > rsum * rsum * T(1.0000000000009095)) continue;
+            const T dist = tsqrt<T>(s2);
+            const T delta = rsum - dist;
+            if (!(delta > zero)) continue;
+            ++nk;
+            if (rj != last_rj) {
+                last_rj = rj;
+                last_req = (ri * rj) / rsum;
+            }
+            const T mag = A.p.kappa * delta - A.p.gamma * tsqrt<T>(last_req * delta);
+            if (dist > zero) {
+                const T sc = mag / dist;
+                fx = fx + sc * dx;
+                fy = fy + sc * dy;
+                fz = fz + sc * dz;
+            } else {
+                degenerate_pair(A.uid[a], A.uid[jc], mag, fx, fy, fz);
+                ++nd;
+            }
+        }
+        // _write_displacement, kernels.py:266-277
+        const T norm = tsqrt<T>(fx * fx + fy * fy + fz * fz);
+        T ddx = zero, ddy = zero, ddz = zero;
+        if (!(norm <= A.p.adh_scale * A.adh[a])) {
+            T sc = A.p.timestep;
+            if (norm * sc > A.p.max_disp) sc = A.p.max_disp / norm;
+            ddx = fx * sc;
+            ddy = fy * sc;
+            ddz = fz * sc;
+        }
+        A.disp_x[a] = ddx;
+        A.disp_y[a] = ddy;
+        A.disp_z[a] = ddz;
+        dmax2 = (float)((double)ddx * ddx + (double)ddy * ddy + (double)ddz * ddz);
+        if (A.new_rec) {
+            const T nxp = xi + ddx, nyp = yi + ddy, nzp = zi + ddz;
+            Rec<T> nr;
+            nr.x = nxp;
+            nr.y = nyp;
+            nr.z = nzp;
+            nr.d = me.d;
+            A.new_rec[a] = nr;
+            const double p3[3] = {(double)nxp, (double)nyp, (double)nzp};
+            unsigned long long *slot = A.slots + (blockIdx.x % kSlots) * kSlotWords;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (p3[q] <= A.shell_lo[q]) atomicMin(slot + q, enc_ordered(p3[q]));
+                if (p3[q] >= A.shell_hi[q]) atomicMax(slot + 3 + q, enc_ordered(p3[q]));
+            }
+        }
+        if (A.rec_m) {
+            A.rec_m[a] = m;
+            A.rec_nk[a] = nk;
+        }
+        c_m = (unsigned)m;
+        c_nk = (unsigned)nk;
+        c_nd = (unsigned)nd;
+    }
+    warp_counters(A.slots, c_m, c_nk, c_nd);
+    warp_dmax(A.slots, dmax2);
+}
+
+}  // namespace cg

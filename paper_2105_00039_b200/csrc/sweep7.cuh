@@ -60,7 +60,15 @@ struct Sweep7Args {
     int n_owned;                // storage indices >= n_owned are ghosts (slab halo): not targets
     int own_lo;                 // targets are storage indices [own_lo, own_lo + n_owned): a relaid
                                 // slab sub-grid keeps its lo ghosts in front of the owned agents
+    // neighbour lists (LIST builds): partners within ri + rj + skin, uid order
+    int *nbr;                   // [kListCap][nbr_stride] storage indices
+    int *nbr_n;                 // per storage index
+    long long nbr_stride;
+    T skin;
+    float skin_f;               // skin rounded up, for the prefilter reach
 };
+
+constexpr int kListCap = 48;    // list entries per agent (more: the list set is not used)
 
 // slot -> storage index: the idx map, or the slot itself (relaid storage)
 template <typename A_t>
@@ -105,9 +113,13 @@ __device__ __forceinline__ void f2_unpack(f32x2 v, float &lo, float &hi)
 // cut at z + reach; FLUSH: evaluate the list whenever it fills (stencil order).
 // DEFER: an agent with more than KS survivors is handed to the overflow
 // kernel (slot appended to A.ovf) instead of taking further walks here.
-template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, bool DEFER>
+// LIST: also record every partner within ri + rj + skin (uid order) in the
+// agent's neighbour list; the walk then covers the 5x5x5 box stencil (a
+// partner within ri + rmax + skin <= 2L can sit two boxes away), while m still
+// counts the reference's 27 boxes.
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, bool DEFER, bool LIST = false>
 __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s, unsigned &c_m,
-                                            unsigned &c_nk, unsigned &c_nd)
+                                            unsigned &c_nk, unsigned &c_nd, float &dmax2)
 {
     __shared__ int lst[KS][kThreads];
     __shared__ uint64_t ukey[UIDMODE ? KS : 1][kThreads];
@@ -125,11 +137,18 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         const float mex = __ldg(myp), mey = __ldg(myp + 2), mez = __ldg(myp + 4);
         const float Lf = (float)A.g.L;
         const Rec<T> me = A.rec[a];
-        const float reach = (float)(me.d * half) + A.rmax + A.margin;
+        const float reach = (float)(me.d * half) + A.rmax + A.margin + (LIST ? A.skin_f : 0.f);
         const float reach2 = reach * reach;
         const float zhi = mez + reach;
         const f32x2 mz2 = f2_splat(mez);
-        const int z0 = max(iz - 1, 0), z1 = min(iz + 1, A.g.dimz - 1);
+        constexpr int R = LIST ? 2 : 1;
+        const int z0m = max(iz - 1, 0), z1m = min(iz + 1, A.g.dimz - 1);
+        int z0 = z0m, z1 = z1m;
+        if (LIST) {   // the boxes two away in z only when the reach crosses the box face
+            const float zl = mez - (float)iz * Lf;
+            if (zl < reach - Lf) z0 = max(iz - 2, 0);
+            if (Lf - zl < reach - Lf) z1 = min(iz + 2, A.g.dimz - 1);
+        }
         // slot pair q = ta / 2 lives in 16-byte words 2q (x pair, y pair) and 2q + 1 (z pair)
         const ulonglong2 *PR = reinterpret_cast<const ulonglong2 *>(A.prox.p);
 
@@ -139,19 +158,32 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         auto walk = [&](auto &&visit, auto &&after) -> int {
             int mm = -1;
 #pragma unroll 1
-            for (int ox = -1; ox <= 1; ++ox) {
+            for (int ox = -R; ox <= R; ++ox) {
                 const int nx = ix + ox;
                 if ((unsigned)nx >= (unsigned)A.g.dimx) continue;
-                const float gx = ox == 0 ? 0.f : fmaxf(0.f, ox < 0 ? mex : Lf - mex);
+                const float gx = ox == 0 ? 0.f
+                                         : fmaxf(0.f, (ox < 0 ? mex : Lf - mex) + (float)(abs(ox) - 1) * Lf);
+                if (LIST && (ox == -2 || ox == 2) && gx * gx > reach2) continue;   // plane out of reach
                 const f32x2 mx2 = f2_splat(mex - (float)ox * Lf);
 #pragma unroll 1
-                for (int oy = -1; oy <= 1; ++oy) {
+                for (int oy = -R; oy <= R; ++oy) {
                     const int ny = iy + oy;
                     if ((unsigned)ny >= (unsigned)A.g.dimy) continue;
+                    if (LIST && (ox == -2 || ox == 2 || oy == -2 || oy == 2)) {
+                        // outer ring: no part of m, skipped unless within reach
+                        const float gy2 = fmaxf(0.f, (oy < 0 ? mey : Lf - mey) + (float)(abs(oy) - 1) * Lf);
+                        const float gyy = oy == 0 ? 0.f : gy2;
+                        if (gx * gx + gyy * gyy > reach2) continue;
+                    }
                     const int base = (nx * A.g.dimy + ny) * A.g.dimz;
                     const int t0 = __ldg(A.off + base + z0), t1 = __ldg(A.off + base + z1 + 1);
-                    mm += t1 - t0;
-                    const float gy = oy == 0 ? 0.f : fmaxf(0.f, oy < 0 ? mey : Lf - mey);
+                    if (!LIST) {
+                        mm += t1 - t0;
+                    } else if (abs(ox) <= 1 && abs(oy) <= 1) {
+                        mm += __ldg(A.off + base + z1m + 1) - __ldg(A.off + base + z0m);
+                    }
+                    const float gy = oy == 0 ? 0.f
+                                             : fmaxf(0.f, (oy < 0 ? mey : Lf - mey) + (float)(abs(oy) - 1) * Lf);
                     if (gx * gx + gy * gy > reach2) continue;
                     const f32x2 my2 = f2_splat(mey - (float)oy * Lf);
                     // two slot pairs per iteration (both loads in flight); the proxy
@@ -202,7 +234,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         const T xi = me.x, yi = me.y, zi = me.z;
         const T ri = me.d * half;
         T fx = zero, fy = zero, fz = zero;
-        int nk = 0, nd = 0;
+        int nk = 0, nd = 0, nl = 0;
         T last_rj = T(-1), last_req = zero;
         // phase 2 for list entries [0, cnt), in list order; the next entry's
         // record is in flight while the current pair is evaluated
@@ -226,6 +258,10 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 const T rj = co.d * half;
                 const T dist = tsqrt<T>(dx * dx + dy * dy + dz * dz);
                 const T rsum = ri + rj;
+                if (LIST && dist <= rsum + A.skin) {
+                    if (nl < kListCap) A.nbr[nl * A.nbr_stride + a] = jc;
+                    ++nl;
+                }
                 const T delta = rsum - dist;
                 if (!(delta > zero)) continue;
                 ++nk;                                                    // kernels.py:230-257
@@ -365,6 +401,11 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         A.disp_x[a] = ddx;
         A.disp_y[a] = ddy;
         A.disp_z[a] = ddz;
+        if (LIST) {
+            A.nbr_n[a] = nl;
+            if (nl > kListCap) atomicAdd(A.slots + (blockIdx.x % kSlots) * kSlotWords + 10, 1ull);
+            dmax2 = fmaxf(dmax2, (float)((double)ddx * ddx + (double)ddy * ddy + (double)ddz * ddz));
+        }
         if (A.new_rec) {               // engine.py:325-327 (separate buffer: two-phase)
             const T nxp = xi + ddx, nyp = yi + ddy, nzp = zi + ddz;
             Rec<T> nr;
@@ -410,25 +451,39 @@ __device__ __forceinline__ void warp_counters(unsigned long long *slots, unsigne
     }
 }
 
-template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, int MINB>
+// the largest squared displacement of the step (neighbour-list validity),
+// one atomic per warp into the block's slot
+__device__ __forceinline__ void warp_dmax(unsigned long long *slots, float dmax2)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax2 = fmaxf(dmax2, __shfl_xor_sync(0xffffffffu, dmax2, o));
+    if ((threadIdx.x & 31) == 0 && dmax2 > 0.f)
+        atomicMax(slots + (blockIdx.x % kSlots) * kSlotWords + 9, enc_ordered((double)dmax2));
+}
+
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, int MINB, bool LIST = false>
 __global__ void __launch_bounds__(kThreads, MINB) sweep7_kernel(Sweep7Args<T> A)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
-    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true>(A, s, c_m, c_nk, c_nd);
+    float dmax2 = 0.f;
+    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true, LIST>(A, s, c_m, c_nk, c_nd, dmax2);
     warp_counters(A.slots, c_m, c_nk, c_nd);
+    if (LIST) warp_dmax(A.slots, dmax2);
 }
 
 // agents deferred by sweep7_kernel (more than KS survivors): grid-stride over
 // the device-side list, further walks per agent
-template <typename T, bool UIDMODE, bool ZSORTED, int KS>
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool LIST = false>
 __global__ void __launch_bounds__(kThreads) sweep7_overflow(Sweep7Args<T> A)
 {
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
+    float dmax2 = 0.f;
     const unsigned cnt = *A.ovf_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
-        sweep_agent<T, UIDMODE, ZSORTED, KS, false, false>(A, A.ovf[k], c_m, c_nk, c_nd);
+        sweep_agent<T, UIDMODE, ZSORTED, KS, false, false, LIST>(A, A.ovf[k], c_m, c_nk, c_nd, dmax2);
     warp_counters(A.slots, c_m, c_nk, c_nd);
+    if (LIST) warp_dmax(A.slots, dmax2);
 }
 
 }  // namespace cg

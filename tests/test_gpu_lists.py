@@ -1,0 +1,108 @@
+"""Neighbour-list reuse (csrc/list.cuh) changes nothing observable: the same
+pool stepped with lists (auto skin, and a small explicit skin that forces
+frequent rebuilds) and without (CG_OPT_LIST_SKIN = 0) gives bit-identical
+counters, grid statistics, storage order, per-agent m / nk, displacements and
+positions at every step -- and list steps really ran.  Anchored to the
+reference through the C oracle on the first steps."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+PARAMS5 = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
+
+
+def _pools():
+    from paper_2105_00039_b200.pool import AgentPool, PrecisionMode
+    from paper_2105_00039_b200.workloads import jittered_lattice_positions
+    yield "lattice", AgentPool.from_arrays(jittered_lattice_positions(24, 8.0, 1.0, 0), 10.0, 0.4)
+    rng = np.random.default_rng(3)
+    # sparse pools (about 1.5 agents per box: the path lists apply to)
+    side = 10.0 * (30000 / 1.5) ** (1 / 3)
+    yield "random", AgentPool.from_arrays(rng.uniform(0, side, (30000, 3)), 10.0, 0.4)
+    yield "hetero", AgentPool.from_arrays(rng.uniform(0, 250.0, (20000, 3)), rng.uniform(4.0, 12.0, 20000),
+                                          rng.uniform(0.0, 1.0, 20000))
+    yield "lattice_f32", AgentPool.from_arrays(jittered_lattice_positions(20, 8.0, 1.0, 1), 10.0, 0.4,
+                                               PrecisionMode.FP32)
+
+
+POOLS = list(_pools())
+
+
+def _run(pool, skin, steps, summation, sort_every=1, freeze_at=()):
+    from paper_2105_00039_b200 import _native as N
+    ctx = N.Context(0, pool.dtype)
+    ctx.set_option(N.CG_OPT_SUMMATION, summation)
+    ctx.set_option(N.CG_OPT_LIST_SKIN, skin)
+    ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+    out = []
+    for k in range(steps):
+        flags = N.CG_STEP_RECORD
+        if sort_every and k % sort_every == 0:
+            flags |= N.CG_STEP_SORT
+        if k in freeze_at:
+            flags |= N.CG_STEP_FREEZE
+        st = ctx.step(PARAMS5, None, 1 << 24, flags)
+        cols = ctx.download()
+        m, nk = ctx.record_export()
+        nb = int(np.prod(list(st.grid_dims)))
+        bi, bc = ctx.grid_export(nb)
+        out.append(((st.force_evals, st.candidates, st.degenerate_pairs, st.grid_occupied_boxes,
+                     st.grid_max_occupancy, tuple(st.grid_dims)), cols, m, nk, bi, bc))
+    stats = ctx.list_stats()
+    ctx.close()
+    return out, stats
+
+
+@pytest.mark.parametrize("summation", [0, 1])
+@pytest.mark.parametrize("name,pool", POOLS, ids=[p[0] for p in POOLS])
+def test_lists_change_nothing(cuda_required, name, pool, summation):
+    steps = 10
+    ref, s0 = _run(pool, 0, steps, summation)
+    assert s0["list_steps"] == 0
+    for skin in (-1, 300):
+        got, s1 = _run(pool, skin, steps, summation, freeze_at=(4,))
+        ref2, _ = _run(pool, 0, steps, summation, freeze_at=(4,))
+        if name.startswith("lattice"):     # small motions: the lists serve steps
+            assert s1["list_steps"] > 0, (name, skin, s1)
+        else:                              # deep random overlaps: lists are built and expire
+            assert s1["builds"] > 0, (name, skin, s1)
+        for k, (a, b) in enumerate(zip(got, ref2)):
+            assert a[0] == b[0], (name, skin, k)
+            for col in a[1]:
+                assert np.array_equal(a[1][col], b[1][col]), (name, skin, k, col)
+            for q in range(2, 6):
+                assert np.array_equal(a[q], b[q]), (name, skin, k, q)
+    # unsorted steps (storage order kept) and the lists-off run agree too
+    got, s2 = _run(pool, -1, 6, summation, sort_every=0)
+    ref3, _ = _run(pool, 0, 6, summation, sort_every=0)
+    for a, b in zip(got, ref3):
+        assert a[0] == b[0]
+        for col in a[1]:
+            assert np.array_equal(a[1][col], b[1][col])
+
+
+def test_lists_match_oracle(cuda_required):
+    """lattice pool, 6 chained steps in uid order: lists-on device == C oracle."""
+    from paper_2105_00039_b200 import _native as N
+    from paper_2105_00039_b200.mechanics import ForceParams
+    pool = POOLS[0][1]
+    ref = pool.copy()
+    ctx = N.Context(0, pool.dtype)
+    ctx.set_option(N.CG_OPT_SUMMATION, 0)
+    ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+    for k in range(6):
+        st = ctx.step(PARAMS5, None, 1 << 24, N.CG_STEP_SORT)
+        r = oracle.step(ref, ForceParams(), sort=True, threads=8)
+        assert (st.force_evals, st.candidates, st.degenerate_pairs) == (
+            r.force_evals, r.candidates, r.degenerate_pairs)
+        cols = ctx.download()
+        assert np.array_equal(cols["uid"], ref.uid)
+        for a, b in (("px", "position_x"), ("py", "position_y"), ("pz", "position_z"),
+                     ("dx", "displacement_x"), ("dy", "displacement_y"), ("dz", "displacement_z")):
+            assert np.array_equal(cols[a], getattr(ref, b)), (k, a)
+    assert ctx.list_stats()["list_steps"] >= 3
+    ctx.close()
