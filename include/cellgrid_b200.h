@@ -56,7 +56,7 @@ extern "C" {
 #define CG_OPT_RELAYOUT_EVERY 4 /* move the records into slot order on every k-th sort step (k >= 1, default 1) */
 #define CG_OPT_PATH 5           /* 0 = auto (by agents per box), 1 = sparse (uid-sorted survivor lists),
                                    2 = dense (boxes ordered by (z, uid), CG_OPT_SUMMATION applies) */
-#define CG_OPT_LIST_SKIN 6      /* neighbour-list reuse on the sparse path: -1 = auto (skin 0.1 x box
+#define CG_OPT_LIST_SKIN 6      /* neighbour-list reuse on the sparse path: -1 = auto (skin 0.07 x box
                                    length, default), 0 = off, k > 0 = skin of k/1000 length units.
                                    Results are identical with or without it (csrc/list.cuh). */
 

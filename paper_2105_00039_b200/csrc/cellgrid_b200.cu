@@ -102,6 +102,8 @@ struct cg_context {
     unsigned long long *stat_dev = nullptr, *stat_host = nullptr;
     cg_step_stats ring[kRing];
     cudaEvent_t ev[kRing][5];
+    cudaStream_t copy_stream = nullptr;       // download: D2H overlapped with the unpack kernels
+    cudaEvent_t dl_ready[9] = {}, dl_done[9] = {}, dl_start = nullptr;
     int64_t steps_done = 0;
     int64_t launches = 0;
     // grid / layout state
@@ -113,7 +115,7 @@ struct cg_context {
     bool last_record = false;
     bool last_dense = false;
     bool grid_current = false;    // the grid indexes the stored positions (cg_build_grid)
-    // neighbour-list reuse (list.cuh): skin < 0 = auto (0.1 x box length), 0 = off
+    // neighbour-list reuse (list.cuh): skin < 0 = auto (0.07 x box length), 0 = off
     double list_skin = -1.0;
     int *nbr = nullptr, *nbr_n = nullptr;
     int64_t nbr_cap = 0;
@@ -854,7 +856,7 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
         if (c->list_wait > 0) c->list_wait--;
         if (build) {
             if ((rc = ensure_lists(c))) return rc;
-            c->list_skin_used = c->list_skin < 0 ? 0.1 * g.L : c->list_skin;
+            c->list_skin_used = c->list_skin < 0 ? 0.07 * g.L : c->list_skin;
             build = c->list_skin_used > 0 && c->list_skin_used <= g.L;
         }
         if ((rc = build_grid_geo<T>(c, g, relayout, sort))) return rc;
@@ -1238,6 +1240,12 @@ void cg_destroy(cg_context *c)
         for (int e = 0; e < 5; ++e)
             if (c->ev[r][e]) cudaEventDestroy(c->ev[r][e]);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (int k = 0; k < 9; ++k) {
+        if (c->dl_ready[k]) cudaEventDestroy(c->dl_ready[k]);
+        if (c->dl_done[k]) cudaEventDestroy(c->dl_done[k]);
+    }
+    if (c->dl_start) cudaEventDestroy(c->dl_start);
     delete c;
 }
 
@@ -1363,30 +1371,66 @@ int cg_download(cg_context *c, void *px, void *py, void *pz, void *diameter, voi
     if (n == 0) return CG_OK;
     int rc = materialize_presentation(c);
     if (rc) return rc;
+    if (!c->copy_stream) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < 9; ++k) {
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_ready[k], cudaEventDisableTiming));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_done[k], cudaEventDisableTiming));
+        }
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_start, cudaEventDisableTiming));
+    }
     void *dst[9] = {px, py, pz, diameter, adherence, uid, dx, dy, dz};
     const void *src[9] = {nullptr, nullptr, nullptr, nullptr, c->b.adh[c->cur_attr], c->b.uid[c->cur_attr],
                           c->b.disp[0], c->b.disp[1], c->b.disp[2]};
-    cudaStream_t st = c->stream;
+    cudaStream_t st = c->stream, cs = c->copy_stream;
     const int *pres = c->pres_state == PRES_IDENTITY ? nullptr : c->b.pres;
+    // staging ring (8 n bytes each): the download buffer and the idle record
+    // buffer (the next step's output); column k is produced on the context
+    // stream into ring[k % R] and copied on the copy stream, so the unpack /
+    // reorder kernels run under the PCIe transfers
+    char *ring[5];
+    int R = 0;
+    ring[R++] = (char *)c->b.stage;
+    const size_t colb = 8 * (size_t)n;
+    for (size_t off = 0; off + colb <= 4 * c->esz * (size_t)c->cap && R < 5; off += colb)
+        ring[R++] = (char *)c->b.rec[1 - c->cur_pos] + off;
+    CUDA_TRY(c, cudaEventRecord(c->dl_start, st));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->dl_start, 0));
+    int used = 0;
     for (int k = 0; k < 9; ++k) {
         if (!dst[k]) continue;
-        if (k < 4) {   // record components, in the reference's order, through the staging buffer
+        const size_t w = k == 5 ? 8 : c->esz;
+        if (k >= 4 && !pres) {   // storage order is the reference's: straight copy
+            CUDA_TRY(c, cudaMemcpyAsync(dst[k], src[k], w * n, cudaMemcpyDeviceToHost, cs));
+            continue;
+        }
+        const int slot = used % R;
+        if (used >= R) CUDA_TRY(c, cudaStreamWaitEvent(st, c->dl_done[used - R], 0));
+        void *buf = ring[slot];
+        if (k < 4) {   // record components
             if (c->prec == CG_FP64)
                 unpack_component<double><<<cdiv(n, kThreads), kThreads, 0, st>>>(
-                    (int)n, (const Rec<double> *)c->b.rec[c->cur_pos], k, pres, (double *)c->b.stage);
+                    (int)n, (const Rec<double> *)c->b.rec[c->cur_pos], k, pres, (double *)buf);
             else
                 unpack_component<float><<<cdiv(n, kThreads), kThreads, 0, st>>>(
-                    (int)n, (const Rec<float> *)c->b.rec[c->cur_pos], k, pres, (float *)c->b.stage);
-            LAUNCH_CHECK(c);
-            c->launches += 1;
-            CUDA_TRY(c, cudaMemcpyAsync(dst[k], c->b.stage, c->esz * n, cudaMemcpyDeviceToHost, st));
-        } else if ((rc = download_column(c, src[k], dst[k], k == 5 ? 8 : c->esz))) {
-            return rc;
+                    (int)n, (const Rec<float> *)c->b.rec[c->cur_pos], k, pres, (float *)buf);
+        } else if (w == 8) {
+            scatter_by<unsigned long long><<<cdiv(n, kThreads), kThreads, 0, st>>>(
+                (int)n, pres, (const unsigned long long *)src[k], (unsigned long long *)buf);
+        } else {
+            scatter_by<unsigned><<<cdiv(n, kThreads), kThreads, 0, st>>>((int)n, pres, (const unsigned *)src[k],
+                                                                          (unsigned *)buf);
         }
-        if (k < 4 || c->pres_state != PRES_IDENTITY)   // the staging buffer is reused per column
-            CUDA_TRY(c, cudaStreamSynchronize(st));
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        CUDA_TRY(c, cudaEventRecord(c->dl_ready[used], st));
+        CUDA_TRY(c, cudaStreamWaitEvent(cs, c->dl_ready[used], 0));
+        CUDA_TRY(c, cudaMemcpyAsync(dst[k], buf, w * n, cudaMemcpyDeviceToHost, cs));
+        CUDA_TRY(c, cudaEventRecord(c->dl_done[used], cs));
+        ++used;
     }
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(cs));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
     return CG_OK;
 }
 
