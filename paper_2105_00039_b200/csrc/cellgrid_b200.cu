@@ -126,6 +126,8 @@ struct cg_context {
     double list_skin_used = 0.0;
     int list_life = 0, list_backoff = 0, list_wait = 0;
     int64_t list_builds = 0, list_steps = 0;
+    bool uid32 = false;           // every stored uid < 2^32 (set at upload; slab exchanges clear it)
+    unsigned long long *maxuid_dev = nullptr;
     int rot = 0;                  // relaid slab sub-grid: slot s lives at storage s - rot (lo ghosts in
                                   // the buffers' front headroom, owned agents at [0, n_owned))
     int64_t sort_steps = 0;
@@ -475,7 +477,7 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
             CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
         } else {
             place_full<T><<<nblk, kThreads, 0, st>>>(n, g, c->bd, c->b.key_rank, c->offset, rec, c->b.idx,
-                                                     c->b.skey, c->b.P(), pk);
+                                                     c->b.skey, c->b.P(), pk, c->b.uid[a]);
             LAUNCH_CHECK(c);
             c->launches += 1;
             CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
@@ -669,6 +671,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     A.ovf_count = c->ovf_count;
     A.n_owned = (int)c->n_owned;
     A.own_lo = c->rot;
+    A.uid32 = c->uid32;
     if (build_lists && !c->last_dense) {
         A.nbr = c->nbr;
         A.nbr_n = c->nbr_n;
@@ -995,8 +998,10 @@ static int slab_plan_t(cg_context *c, const double bb[7], double ir, int64_t box
             return fail(c, CG_ERR_GRID_OVERFLOW, "slab sub-grid of %lld boxes exceeds cap %lld",
                         (long long)sub, (long long)box_cap);
     }
-    // every candidate radius is bounded by the global largest diameter
+    // every candidate radius is bounded by the global largest diameter;
+    // arrivals and ghosts bring uids this context has not seen
     c->max_diam = std::max(c->max_diam, bb[6]);
+    c->uid32 = false;
     planes[0] = S.x0;
     planes[1] = S.x1;
     cudaStream_t st = c->stream;
@@ -1231,7 +1236,8 @@ void cg_destroy(cg_context *c)
     int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->moff};
     for (int *p : ptrs)
         if (p) cudaFree(p);
-    void *vptrs[] = {c->scan_status, c->slots, c->maxd_enc, c->ovf_count, c->block_counters, c->bbox_dev, c->stat_dev};
+    void *vptrs[] = {c->scan_status, c->slots, c->maxd_enc, c->ovf_count, c->block_counters, c->bbox_dev, c->stat_dev,
+                     c->maxuid_dev};
     for (void *p : vptrs)
         if (p) cudaFree(p);
     if (c->bbox_host) cudaFreeHost(c->bbox_host);
@@ -1347,6 +1353,9 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
                                                        (Rec<float> *)c->b.rec[0]);
     for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMemsetAsync(c->b.disp[a], 0, fe, st));
     CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, sizeof(unsigned long long), st));
+    if (!c->maxuid_dev) CUDA_TRY(c, cudaMalloc(&c->maxuid_dev, sizeof(unsigned long long)));
+    CUDA_TRY(c, cudaMemsetAsync(c->maxuid_dev, 0, sizeof(unsigned long long), st));
+    max_uid_kernel<<<std::min(kBboxBlocks, nblk), kThreads, 0, st>>>((int)n, c->b.uid[0], c->maxuid_dev);
     if (c->prec == CG_FP64)
         max_diam_kernel<double><<<std::min(kBboxBlocks, nblk), kThreads, 0, st>>>(
             (int)n, (const Rec<double> *)c->b.rec[0], c->maxd_enc);
@@ -1354,11 +1363,13 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
         max_diam_kernel<float><<<std::min(kBboxBlocks, nblk), kThreads, 0, st>>>(
             (int)n, (const Rec<float> *)c->b.rec[0], c->maxd_enc);
     LAUNCH_CHECK(c);
-    c->launches += 2;
-    unsigned long long enc = 0;
+    c->launches += 3;
+    unsigned long long enc = 0, mu = 0;
     CUDA_TRY(c, cudaMemcpyAsync(&enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaMemcpyAsync(&mu, c->maxuid_dev, sizeof mu, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));   // host buffers are only borrowed
     c->max_diam = dec_ordered(enc);
+    c->uid32 = mu < (1ull << 32);
     return CG_OK;
 }
 

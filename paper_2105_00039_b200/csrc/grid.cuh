@@ -192,6 +192,18 @@ __global__ void max_diam_kernel(int n, const Rec<T> *__restrict__ rec, unsigned 
     if ((threadIdx.x & 31) == 0 && v != -INFINITY) atomicMax(out, enc_ordered(v));
 }
 
+// max(uid) once per upload: every uid below 2^32 lets the sweep take its
+// survivor sort keys from the proxies
+__global__ void max_uid_kernel(int n, const uint64_t *__restrict__ uid, unsigned long long *__restrict__ out)
+{
+    unsigned long long v = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        v = max(v, (unsigned long long)uid[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
 // ---------------------------------------------------------------- K5 Morton table
 // mrank[flat] = Morton rank of the box, minv[rank] = flat.  Rebuilt only when
 // the grid dims change (presentation order only).
@@ -595,7 +607,9 @@ __global__ void __launch_bounds__(kThreads) place(int n, const int2 *__restrict_
 // fp32 proxies in slot order, one 32-byte record per slot pair so the sweep
 // loads two candidates with one sector pair and tests them with one packed
 // FADD2/FFMA2 chain:
-//   p[8q .. 8q+7] = (x_2q, x_2q+1, y_2q, y_2q+1, z_2q, z_2q+1, -, -)
+//   p[8q .. 8q+7] = (x_2q, x_2q+1, y_2q, y_2q+1, z_2q, z_2q+1, u_2q, u_2q+1)
+// u = the low 32 bits of the uid (the survivor sort key when every uid is
+// below 2^32 -- the sweep then never loads the uid column).
 // x/y box-local (|err| <= ulp(L)), z grid-relative (monotone, so z-sorted
 // boxes stay sorted).  The candidate's radius is not stored: the sweep bounds
 // it by the pool's largest radius (conservative).
@@ -604,12 +618,14 @@ struct Proxies {
 };
 
 template <typename T>
-__device__ __forceinline__ void put_proxy(const Proxies &P, const Geometry &g, int s, int ix, int iy, T x, T y, T z)
+__device__ __forceinline__ void put_proxy(const Proxies &P, const Geometry &g, int s, int ix, int iy, T x, T y, T z,
+                                          uint64_t uid)
 {
     float *r = P.p + 8 * (s >> 1) + (s & 1);
     r[0] = (float)((double)x - (g.ox + (double)(ix + g.xoff) * g.L));
     r[2] = (float)((double)y - (g.oy + (double)iy * g.L));
     r[4] = (float)((double)z - g.oz);
+    reinterpret_cast<unsigned *>(r)[6] = (unsigned)uid;
 }
 
 // Members of a box are re-ranked by (z, uid) -- a pure function of the
@@ -643,7 +659,7 @@ __global__ void __launch_bounds__(kThreads) order_gather(
     int ix, iy, iz;
     decode_box(bd, k, ix, iy, iz);
     skey[dst] = k;
-    put_proxy<T>(prox, g, dst, ix, iy, ri.x, ri.y, zi);
+    put_proxy<T>(prox, g, dst, ix, iy, ri.x, ri.y, zi, ui);
     if (RELAYOUT) {
         orec[dst] = ri;
         oadh[dst] = adh[i];
@@ -665,7 +681,8 @@ __global__ void __launch_bounds__(kThreads) place_full(int n, Geometry g, BoxDec
                                                        const int2 *__restrict__ key_rank,
                                                        const int *__restrict__ offset, const Rec<T> *__restrict__ rec,
                                                        int *__restrict__ idx, int *__restrict__ skey,
-                                                       Proxies prox, int *__restrict__ pkey)
+                                                       Proxies prox, int *__restrict__ pkey,
+                                                       const uint64_t *__restrict__ uid)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -676,7 +693,7 @@ __global__ void __launch_bounds__(kThreads) place_full(int n, Geometry g, BoxDec
     idx[slot] = i;
     skey[slot] = kr.x;
     const Rec<T> r = rec[i];
-    put_proxy<T>(prox, g, slot, ix, iy, r.x, r.y, r.z);
+    put_proxy<T>(prox, g, slot, ix, iy, r.x, r.y, r.z, uid[i]);
     if (pkey) pkey[i] = kr.x;
 }
 
@@ -697,7 +714,7 @@ __global__ void __launch_bounds__(kThreads) place_relayout(
     decode_box(bd, kr.x, ix, iy, iz);
     const Rec<T> r = rec[i];
     skey[slot] = kr.x;
-    put_proxy<T>(prox, g, slot, ix, iy, r.x, r.y, r.z);
+    put_proxy<T>(prox, g, slot, ix, iy, r.x, r.y, r.z, uid[i]);
     orec[slot] = r;
     oadh[slot] = adh[i];
     ouid[slot] = uid[i];

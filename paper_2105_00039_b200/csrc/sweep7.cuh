@@ -58,6 +58,7 @@ struct Sweep7Args {
     int *ovf;                   // slots of agents deferred to the overflow kernel
     unsigned *ovf_count;
     int n_owned;                // storage indices >= n_owned are ghosts (slab halo): not targets
+    bool uid32;                 // every uid < 2^32: survivor sort keys come from the proxies
     int own_lo;                 // targets are storage indices [own_lo, own_lo + n_owned): a relaid
                                 // slab sub-grid keeps its lo ghosts in front of the owned agents
     // neighbour lists (LIST builds): partners within ri + rj + skin, uid order
@@ -214,10 +215,10 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                             const bool p1 = a1 <= reach2 && ta + 1 < t1;
                             const bool p2 = b0 <= reach2 && ta + 2 < t1;
                             const bool p3 = b1 <= reach2 && ta + 3 < t1;
-                            if (p0) visit(ta);
-                            if (p1) visit(ta + 1);
-                            if (p2) visit(ta + 2);
-                            if (p3) visit(ta + 3);
+                            if (p0) visit(ta, (unsigned)za.y);
+                            if (p1) visit(ta + 1, (unsigned)(za.y >> 32));
+                            if (p2) visit(ta + 2, (unsigned)zb.y);
+                            if (p3) visit(ta + 3, (unsigned)(zb.y >> 32));
                             after();
                         }
                         if (ZSORTED) {
@@ -292,7 +293,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         if (!UIDMODE && FLUSH) {
             // dense neighbourhoods: the list is evaluated whenever it fills up
             int ns = 0;
-            m = walk([&](int t) { LST(ns++) = t; },
+            m = walk([&](int t, unsigned) { LST(ns++) = t; },
                      [&]() {
                          if (ns > KS - 4) {   // a batch appends up to 4
                              evaluate(ns);
@@ -305,7 +306,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             // collecting the next KS (walk order is deterministic)
             int ns = 0, total = 0;
             m = walk(
-                [&](int t) {
+                [&](int t, unsigned) {
                     if (ns < KS) LST(ns++) = t;
                     ++total;
                 },
@@ -319,7 +320,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 int seen = 0;
                 ns = 0;
                 walk(
-                    [&](int t) {
+                    [&](int t, unsigned) {
                         if (seen >= done && ns < KS) LST(ns++) = t;
                         ++seen;
                     },
@@ -331,8 +332,12 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             // first walk: keep the first KS survivors, count all of them
             int ns = 0, total = 0;
             m = walk(
-                [&](int t) {
-                    if (ns < KS) LST(ns++) = t;
+                [&](int t, unsigned u) {
+                    if (ns < KS) {
+                        LST(ns) = t;
+                        UKEY(ns) = A.uid32 ? (uint64_t)u : cand_uid(t);
+                        ++ns;
+                    }
                     ++total;
                 },
                 [] {});
@@ -342,7 +347,6 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             }
             if (total <= KS) {
                 // insertion sort by uid, then one evaluation in uid order
-                for (int p = 0; p < ns; ++p) UKEY(p) = cand_uid(LST(p));
                 for (int p = 1; p < ns; ++p) {
                     const uint64_t u = UKEY(p);
                     const int v = LST(p);
@@ -364,8 +368,8 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 while (done < total) {
                     int nr = 0;
                     walk(
-                        [&](int t) {
-                            const uint64_t ut = cand_uid(t);
+                        [&](int t, unsigned u) {
+                            const uint64_t ut = A.uid32 ? (uint64_t)u : cand_uid(t);
                             if (!first && ut <= floor_uid) return;
                             int q;
                             if (nr < KS) q = nr++;
