@@ -7,7 +7,7 @@ executed by hand-written sm_100a kernels behind a C ABI
 """
 
 from .engine import (GrowthParams, Gpu, RunReport, SimulationConfig, StepStats, TileCapacityError,
-                     run, step, strategy_label)
+                     grow_and_divide, run, step, strategy_label)
 from .geometry import FP32, FP64, Aabb
 from .mechanics import DEFAULT_ADHERENCE, FLOPS_PER_FORCE_EVAL, ForceParams
 from .pool import AgentPool, PoolCapacityError, PrecisionMode
@@ -21,4 +21,4 @@ __all__ = ["Aabb", "AgentPool", "DEFAULT_ADHERENCE", "DEFAULT_BOX_CAP", "FLOPS_P
            "FP32", "FP64", "ForceParams", "Gpu", "GridOverflowError", "GrowthParams",
            "PoolCapacityError", "PrecisionMode", "RunReport", "SimulationConfig",
            "StencilTooSmallError", "StepStats", "TileCapacityError", "UniformGrid",
-           "box_side_for_density", "build_grid", "run", "step", "strategy_label"]
+           "box_side_for_density", "build_grid", "grow_and_divide", "run", "step", "strategy_label"]

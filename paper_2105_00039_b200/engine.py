@@ -13,6 +13,13 @@ no CPU path: an unavailable device raises.
 device and writes positions, displacements and the new storage order back into
 the pool.  ``run`` keeps the population resident in HBM for all steps and
 synchronises the host pool once at the end.
+
+The behaviour phase (growth then division, reference engine.py:191-232) runs
+on the host before the device step, with the reference's own numpy
+arithmetic: np.cbrt is the platform libm's (not correctly rounded) and the
+daughter directions are numpy's Philox / ziggurat normal draws, neither of
+which a device kernel reproduces bit for bit.  A run with
+growth therefore synchronises the pool every step.
 """
 
 from __future__ import annotations
@@ -28,6 +35,7 @@ import numpy as np
 from . import _native
 from .mechanics import ForceParams
 from .pool import PrecisionMode
+from .rng import unit_vector
 
 RECORD_SCALARS = 5      # reference engine.py:38-39 (bytes_modeled record)
 DEFAULT_BOX_CAP = 1 << 24
@@ -81,8 +89,8 @@ def strategy_label(strategy):
 
 @dataclass(frozen=True)
 class GrowthParams:
-    """Reference engine.py:100-112.  The behaviour phase is outside the B200
-    path; a config carrying growth is rejected by ``step``."""
+    """Reference engine.py:100-112: volume growth per step and the diameter
+    gate for division (the behaviour phase, ``grow_and_divide``)."""
 
     volume_growth_rate: float
     division_diameter: float
@@ -193,6 +201,46 @@ def _release_contexts():
     _contexts.clear()
 
 
+_SIXTH_PI = np.pi / 6.0
+
+
+def grow_and_divide(pool, growth: GrowthParams, step_index=0):
+    """Behaviour phase (reference engine.py:191-232), host numpy: every agent's
+    volume pi/6 d^3 grows by ``volume_growth_rate`` (pool dtype); agents whose
+    diameter reached ``division_diameter`` split, mothers in ascending uid:
+    the mother keeps half the volume, the daughter (the other half, same
+    adherence) is appended at mother_radius / 4 along ``unit_vector(uid,
+    step_index)``.  Returns the number of divisions."""
+    if pool.count == 0:
+        return 0
+    T = pool.dtype.type
+    k6 = T(_SIXTH_PI)
+    d = pool.diameter
+    vol = k6 * (d * d * d) + T(growth.volume_growth_rate)
+    pool.diameter = np.cbrt(vol / k6)
+    if not growth.division_enabled:
+        return 0
+    ripe = np.flatnonzero(pool.diameter >= T(growth.division_diameter))
+    if ripe.shape[0] == 0:
+        return 0
+    ripe = ripe[np.argsort(pool.uid[ripe])]
+    k = ripe.shape[0]
+    where = np.empty((k, 3), np.float64)
+    half_d = np.empty(k, np.float64)
+    adh = np.empty(k, np.float64)
+    for row, i in enumerate(ripe):
+        dm = pool.diameter[i]
+        dh = np.cbrt((T(0.5) * (k6 * (dm * dm * dm))) / k6)
+        shift = unit_vector(int(pool.uid[i]), step_index) * (float(dm) * 0.5 / 4.0)
+        where[row] = (float(pool.position_x[i]) + shift[0], float(pool.position_y[i]) + shift[1],
+                      float(pool.position_z[i]) + shift[2])
+        half_d[row] = float(dh)
+        adh[row] = float(pool.adherence[i])
+        pool.diameter[i] = dh
+    pool.append_many(where, half_d, adh)
+    return k
+
+
 def params_vector(fp: ForceParams):
     return np.array([fp.kappa, fp.gamma, fp.timestep, fp.max_displacement,
                      fp.adherence_scale], np.float64)
@@ -214,9 +262,6 @@ def _check(pool, config):
     if pool.dtype != config.precision.dtype:
         raise ValueError("pool dtype %s does not match configured precision %s"
                          % (pool.dtype, config.precision.value))
-    if config.growth is not None:
-        raise NotImplementedError("the behaviour phase (growth/division, reference "
-                                  "engine.py:191-232) is not part of the B200 path")
 
 
 def _upload(ctx, pool):
@@ -267,25 +312,40 @@ def _to_stats(st, step_index, itemsize):
 
 
 def step(pool, config: SimulationConfig, step_index=0):
-    """Advance ``pool`` by one mechanical step on the GPU; returns StepStats."""
+    """Advance ``pool`` by one step: the behaviour phase (if configured) on the
+    host, then the mechanical step on the GPU; returns StepStats."""
     _check(pool, config)
+    divisions, t_behavior = 0, 0.0
+    if config.growth is not None and pool.count:
+        t0 = time.perf_counter()
+        divisions = grow_and_divide(pool, config.growth, step_index)
+        t_behavior = time.perf_counter() - t0
     if pool.count == 0:
-        return _empty_stats(step_index)
+        st = _empty_stats(step_index)
+        st.t_behavior = t_behavior
+        return st
     ctx = _context(config.strategy, pool.dtype)
     _upload(ctx, pool)
     st = ctx.step(params_vector(config.force_params), config.interaction_radius,
                   DEFAULT_BOX_CAP, step_flags(config, step_index))
     _download(ctx, pool)
-    return _to_stats(st, step_index, pool.precision.itemsize)
+    out = _to_stats(st, step_index, pool.precision.itemsize)
+    out.divisions = divisions
+    out.t_behavior = t_behavior
+    out.t_total += t_behavior
+    return out
 
 
 def run(pool, config: SimulationConfig):
-    """``config.steps`` steps with the pool resident on the device."""
+    """``config.steps`` steps with the pool resident on the device (synchronised
+    every step when the behaviour phase is on: it runs on the host)."""
     _check(pool, config)
     t0 = time.perf_counter()
     initial = pool.count
     stats = []
-    if pool.count == 0:
+    if config.growth is not None:
+        stats = [step(pool, config, k) for k in range(config.steps)]
+    elif pool.count == 0:
         stats = [_empty_stats(k) for k in range(config.steps)]
     elif config.steps:
         ctx = _context(config.strategy, pool.dtype)

@@ -20,7 +20,7 @@ def pytest_configure(config):
 def golden_names():
     return sorted(os.path.splitext(os.path.basename(p))[0]
                   for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith("nbr_"))   # radius-query tables
+                  if not os.path.basename(p).startswith(("nbr_", "growth_")))   # query / behaviour fixtures
 
 
 def load_golden(name):
