@@ -178,18 +178,6 @@ __global__ void slab_fill_holes(int nmove, const int *__restrict__ holes, const 
     store_record(C, holes[k], rec);
 }
 
-// same, with the hole count read on the device
-template <typename T>
-__global__ void slab_fill_holes_dev(const unsigned *__restrict__ nmove, const int *__restrict__ holes,
-                                    const int *__restrict__ movers, SlabCols<T> C)
-{
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= (int)*nmove) return;
-    SlabRecord<T> rec;
-    load_record(C, movers[k], rec);
-    store_record(C, holes[k], rec);
-}
-
 // received runs -> storage: seg k covers records [start[k], start[k+1]) of the
 // receive buffer and lands at storage dst[k] + (record - start[k])
 struct SlabSegs {
