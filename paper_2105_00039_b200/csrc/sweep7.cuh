@@ -181,7 +181,10 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                     if (!LIST) {
                         mm += t1 - t0;
                     } else if (abs(ox) <= 1 && abs(oy) <= 1) {
-                        mm += __ldg(A.off + base + z1m + 1) - __ldg(A.off + base + z0m);
+                        // the walked run is wider than the 3-box column only near a z face
+                        const int m1 = z1 == z1m ? t1 : __ldg(A.off + base + z1m + 1);
+                        const int m0 = z0 == z0m ? t0 : __ldg(A.off + base + z0m);
+                        mm += m1 - m0;
                     }
                     const float gy = oy == 0 ? 0.f
                                              : fmaxf(0.f, (oy < 0 ? mey : Lf - mey) + (float)(abs(oy) - 1) * Lf);
