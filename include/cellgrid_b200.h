@@ -165,14 +165,20 @@ int cg_neighbor_fill(cg_context *ctx, double radius, const int64_t *indptr, int6
 int64_t cg_record_bytes(const cg_context *ctx);
 /* Pre-size the agent buffers (before cg_upload) for arrivals and ghosts. */
 int cg_reserve(cg_context *ctx, int64_t capacity);
-/* Exact bbox of the owned agents (min xyz, max xyz) + max diameter. */
-int cg_local_bbox(cg_context *ctx, double out[7]);
+/* Exact bbox of the owned agents (min xyz, max xyz), max diameter, the last
+ * step's largest squared displacement and neighbour-list overflow count: all
+ * nine are all-reduced with MAX (after negating the three minima). */
+int cg_local_bbox(cg_context *ctx, double out[9]);
 /* Geometry from the global bbox (spatial.py:99-116; GridOverflowError as
  * cg_step) and slab planes: planes = {X_rank, X_rank+1}.  counts (3 * world):
  * for destination rank q, counts[3q] = owned agents that migrate to q (0 for
- * q == rank), counts[3q+1] = owned agents in plane X_q - 1 (q's lo ghosts),
- * counts[3q+2] = owned agents in plane X_q+1 (q's hi ghosts). */
-int cg_slab_plan(cg_context *ctx, const double bbox[7], double interaction_radius, int64_t box_cap,
+ * q == rank), counts[3q+1] = owned agents in q's ghost band below its slab,
+ * counts[3q+2] = owned agents in q's ghost band above it (band: 1 plane, 3
+ * with neighbour lists).  With neighbour lists, a step whose lists are still
+ * valid (decided identically on every rank from the all-reduced bbox[7..8])
+ * keeps the partition: no migrants, and the ghost runs are the refresh of the
+ * ghosts every rank holds since the last rebuild. */
+int cg_slab_plan(cg_context *ctx, const double bbox[9], double interaction_radius, int64_t box_cap,
                  int world, int rank, int64_t *counts, int64_t planes[2]);
 /* Outgoing records -> send, grouped by destination rank (ascending), each
  * destination's run = [migrants][lo ghosts][hi ghosts] with the cg_slab_plan

@@ -260,7 +260,9 @@ class Context:
         check(load().cg_reserve(self.h, int(capacity)), self.h)
 
     def local_bbox(self):
-        out = np.empty(7, np.float64)
+        """min xyz, max xyz, max diameter, last step's largest squared
+        displacement, last step's neighbour-list overflows (cg_local_bbox)."""
+        out = np.empty(9, np.float64)
         check(load().cg_local_bbox(self.h, ptr(out)), self.h)
         return out
 

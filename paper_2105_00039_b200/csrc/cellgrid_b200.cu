@@ -154,6 +154,23 @@ struct cg_context {
         int64_t h_counts[kHist] = {};
         int64_t steps = 0;
         int64_t ghost_lo = 0;    // ghosts from rank - 1 (in front of the ghost buffer)
+        // neighbour lists across slabs (list mode: frozen partition, ghost refresh)
+        bool list_mode = false;    // this step refreshes ghosts and runs the list sweep
+        bool refresh_ready = false;
+        bool unpacked = false;
+        int64_t n_total = 0;       // owned + ghosts kept between rebuilds
+        int rot_build = 0;         // index of the first owned agent (the lo-ghost count)
+        double x_lo_abs = 0, x_hi_abs = 0;   // the owned slab's x range at the rebuild
+        int64_t ref_counts[kHist] = {};      // refresh records per (destination, kind)
+        int64_t ref_total = 0;
+        int *ref_list = nullptr;             // owned indices, grouped by (destination, kind)
+        unsigned long long *ref_off = nullptr;
+        uint64_t *g_uid = nullptr, *g_uid_sorted = nullptr, *r_uid = nullptr, *r_uid_sorted = nullptr;
+        int *g_idx = nullptr, *g_idx_sorted = nullptr, *r_ord = nullptr, *r_ord_sorted = nullptr;
+        void *sort_tmp = nullptr;
+        size_t sort_tmp_bytes = 0;
+        unsigned *mismatch = nullptr;
+        int64_t list_cap = 0;
     } slab;
     std::string err;
 };
@@ -957,6 +974,60 @@ static int slab_alloc(cg_context *c)
     return CG_OK;
 }
 
+static int slab_list_alloc(cg_context *c)
+{
+    auto &S = c->slab;
+    if (S.list_cap >= c->cap && S.ref_list) return CG_OK;
+    void *ptrs[] = {S.ref_list, S.ref_off, S.g_uid, S.g_uid_sorted, S.r_uid, S.r_uid_sorted, S.g_idx,
+                    S.g_idx_sorted, S.r_ord, S.r_ord_sorted, S.sort_tmp, S.mismatch};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    const size_t n = (size_t)std::max<int64_t>(c->cap, 1);
+    CUDA_TRY(c, cudaMalloc(&S.ref_list, sizeof(int) * n));
+    CUDA_TRY(c, cudaMalloc(&S.ref_off, sizeof(unsigned long long) * kHist));
+    uint64_t **u64[] = {&S.g_uid, &S.g_uid_sorted, &S.r_uid, &S.r_uid_sorted};
+    for (uint64_t **p : u64) CUDA_TRY(c, cudaMalloc(p, sizeof(uint64_t) * n));
+    int **i32[] = {&S.g_idx, &S.g_idx_sorted, &S.r_ord, &S.r_ord_sorted};
+    for (int **p : i32) CUDA_TRY(c, cudaMalloc(p, sizeof(int) * n));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (const int *)nullptr, (int *)nullptr, (int)n, 0, 64, c->stream);
+    CUDA_TRY(c, cudaMalloc(&S.sort_tmp, tb));
+    S.sort_tmp_bytes = tb;
+    CUDA_TRY(c, cudaMalloc(&S.mismatch, sizeof(unsigned)));
+    S.list_cap = c->cap;
+    return CG_OK;
+}
+
+// every slab index i lives at buffer position i - rot (lo ghosts in the headroom)
+template <typename T>
+static SlabCols<T> cols_at(cg_context *c, int rot)
+{
+    SlabCols<T> C;
+    C.rec = (Rec<T> *)c->b.rec[c->cur_pos] - rot;
+    C.adh = (T *)c->b.adh[c->cur_attr] - rot;
+    C.uid = c->b.uid[c->cur_attr] - rot;
+    C.dx = (T *)c->b.disp[0] - rot;
+    C.dy = (T *)c->b.disp[1] - rot;
+    C.dz = (T *)c->b.disp[2] - rot;
+    return C;
+}
+
+// neighbour-list validity from the all-reduced largest displacement (bb[7],
+// squared) and list overflows (bb[8]) of the previous step: every rank takes
+// the same decision
+template <typename T>
+static void slab_list_account(cg_context *c, const double bb[9])
+{
+    double saved[9];
+    for (int k = 0; k < 9; ++k) {
+        saved[k] = c->bbox_host[k];
+        c->bbox_host[k] = bb[k];
+    }
+    list_account<T>(c);
+    for (int k = 0; k < 9; ++k) c->bbox_host[k] = saved[k];
+}
+
 template <typename T>
 static SlabCols<T> cur_cols(cg_context *c)
 {
@@ -971,7 +1042,7 @@ static SlabCols<T> cur_cols(cg_context *c)
 }
 
 template <typename T>
-static int slab_plan_t(cg_context *c, const double bb[7], double ir, int64_t box_cap, int world, int rank,
+static int slab_plan_t(cg_context *c, const double bb[9], double ir, int64_t box_cap, int world, int rank,
                        int64_t *counts, int64_t planes[2])
 {
     auto &S = c->slab;
@@ -985,15 +1056,44 @@ static int slab_plan_t(cg_context *c, const double bb[7], double ir, int64_t box
     if ((rc = host_geometry(c, bb, ir, INT64_MAX, g, dims64, origin))) return rc;
     if (g.dimx < world)
         return fail(c, CG_ERR_VALUE, "grid of %d x-planes is too narrow for %d slabs", g.dimx, world);
+    const bool lists_on = c->list_skin != 0.0 && c->sweep_impl == 1 && world == S.world && rank == S.rank;
+    if (lists_on) slab_list_account<T>(c, bb);
+    S.list_mode = lists_on && c->list_valid && S.refresh_ready && c->nbr_cap == c->cap &&
+                  2.0 * c->list_D <= 0.999 * c->list_skin_used;
+    S.unpacked = false;
     S.g = g;
+    if (S.list_mode) {
+        // frozen partition: the owners refresh the ghosts they hold in other ranks' bands
+        for (int k = 0; k < 3 * world; ++k) counts[k] = (k % 3 == 0) ? 0 : S.ref_counts[k];
+        planes[0] = S.x0;
+        planes[1] = S.x1;
+        S.planned = true;
+        S.packed = false;
+        return CG_OK;
+    }
+    if (c->list_valid && lists_on) {   // expired lists: the same backoff rule as a single context
+        c->list_valid = false;
+        if (c->list_life < 2) {
+            c->list_backoff = c->list_backoff ? std::min(2 * c->list_backoff, 64) : 4;
+            c->list_wait = c->list_backoff;
+        } else {
+            c->list_backoff = 0;
+        }
+    }
+    // a rebuild: the ghosts kept by list steps are dropped
+    c->n = c->n_owned;
+    S.refresh_ready = false;
+    c->list_valid = false;
     S.world = world;
     S.rank = rank;
     S.B.world = world;
+    S.B.band = c->list_skin != 0.0 && c->sweep_impl == 1 ? 3 : 1;
     for (int k = 0; k <= world; ++k) S.B.x[k] = (int)(((int64_t)k * g.dimx) / world);
     S.x0 = S.B.x[rank];
     S.x1 = S.B.x[rank + 1];
     {
-        const int64_t sub = (int64_t)(std::min(S.x1 + 1, g.dimx) - std::max(S.x0 - 1, 0)) * g.dimy * g.dimz;
+        const int64_t sub = (int64_t)(std::min(S.x1 + S.B.band, g.dimx) - std::max(S.x0 - S.B.band, 0)) * g.dimy *
+                            g.dimz;
         if (sub > box_cap)
             return fail(c, CG_ERR_GRID_OVERFLOW, "slab sub-grid of %lld boxes exceeds cap %lld",
                         (long long)sub, (long long)box_cap);
@@ -1028,6 +1128,17 @@ template <typename T>
 static int slab_pack_t(cg_context *c, void *send)
 {
     auto &S = c->slab;
+    if (S.list_mode) {   // refresh records of the owned agents in other ranks' bands, in run order
+        S.packed = true;
+        if (S.ref_total > 0) {
+            slab_refresh_pack<T><<<cdiv(S.ref_total, kThreads), kThreads, 0, c->stream>>>(
+                (int)S.ref_total, S.ref_list, cols_at<T>(c, S.rot_build), (SlabRecord<T> *)send);
+            LAUNCH_CHECK(c);
+            c->launches += 1;
+        }
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        return CG_OK;
+    }
     const int n = (int)c->n_owned;
     const int W = S.world;
     const int n_keep = (int)S.h_counts[3 * W];
@@ -1049,8 +1160,8 @@ static int slab_pack_t(cg_context *c, void *send)
     CUDA_TRY(c, cudaStreamSynchronize(st));
     const SlabCols<T> C = cur_cols<T>(c);
     if (hc[0])
-        slab_pack_out<T><<<cdiv(hc[0], kThreads), kThreads, 0, st>>>((int)hc[0], S.rank, S.out, S.dest, S.seg_off,
-                                                                     S.cursor, C, (SlabRecord<T> *)send);
+        slab_pack_out<T><<<cdiv(hc[0], kThreads), kThreads, 0, st>>>((int)hc[0], S.rank, S.g, S.B, S.out, S.dest,
+                                                                     S.seg_off, S.cursor, C, (SlabRecord<T> *)send);
     if (hc[1])
         slab_fill_holes<T><<<cdiv(hc[1], kThreads), kThreads, 0, st>>>((int)hc[1], S.holes, S.movers, C);
     LAUNCH_CHECK(c);
@@ -1066,6 +1177,38 @@ static int slab_unpack_t(cg_context *c, const void *recv, const int64_t *rc3)
 {
     auto &S = c->slab;
     const int W = S.world;
+    S.unpacked = true;
+    if (S.list_mode) {
+        int64_t got = 0;
+        for (int k = 0; k < 3 * W; ++k) {
+            if (rc3[k] < 0 || (k % 3 == 0 && rc3[k] != 0))
+                return fail(c, CG_ERR_STATE, "unexpected migrants in a ghost-refresh step");
+            got += rc3[k];
+        }
+        const int64_t ng = S.n_total - c->n_owned;
+        if (got != ng)
+            return fail(c, CG_ERR_STATE, "ghost refresh brought %lld records for %lld ghosts", (long long)got,
+                        (long long)ng);
+        if (ng == 0) return CG_OK;
+        cudaStream_t st = c->stream;
+        const int rb = (int)sizeof(SlabRecord<T>);
+        slab_recv_keys<<<cdiv(ng, kThreads), kThreads, 0, st>>>((int)ng, (const unsigned char *)recv, rb,
+                                                                 (int)offsetof(SlabRecord<T>, uid), S.r_uid, S.r_ord);
+        size_t tb = S.sort_tmp_bytes;
+        CUDA_TRY(c, cub::DeviceRadixSort::SortPairs(S.sort_tmp, tb, S.r_uid, S.r_uid_sorted, S.r_ord, S.r_ord_sorted,
+                                                    (int)ng, 0, 64, st));
+        CUDA_TRY(c, cudaMemsetAsync(S.mismatch, 0, sizeof(unsigned), st));
+        slab_refresh_scatter<T><<<cdiv(ng, kThreads), kThreads, 0, st>>>(
+            (int)ng, (const SlabRecord<T> *)recv, S.r_ord_sorted, S.r_uid_sorted, S.g_uid_sorted, S.g_idx_sorted,
+            (Rec<T> *)c->b.rec[c->cur_pos] - S.rot_build, S.mismatch);
+        LAUNCH_CHECK(c);
+        c->launches += 3;
+        unsigned bad = 0;
+        CUDA_TRY(c, cudaMemcpyAsync(&bad, S.mismatch, sizeof bad, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        if (bad) return fail(c, CG_ERR_STATE, "ghost refresh: %u records do not match the ghost set", bad);
+        return CG_OK;
+    }
     int64_t mig = 0, glo = 0, ghi = 0;
     for (int s = 0; s < W; ++s) {
         if (rc3[3 * s] < 0 || rc3[3 * s + 1] < 0 || rc3[3 * s + 2] < 0)
@@ -1107,13 +1250,136 @@ static int slab_unpack_t(cg_context *c, const void *recv, const int64_t *rc3)
     return CG_OK;
 }
 
+// After a rebuild step with lists: the ghost table (ghost indices sorted by
+// uid) and the refresh lists (owned agents in other ranks' bands, by run).
+template <typename T>
+static int slab_list_tables(cg_context *c)
+{
+    auto &S = c->slab;
+    int rc;
+    if ((rc = slab_list_alloc(c))) return rc;
+    cudaStream_t st = c->stream;
+    const int W = S.world, lo = c->rot, no = (int)c->n_owned, nt = (int)c->n;
+    const int ng = nt - no;
+    const SlabCols<T> C = cols_at<T>(c, lo);   // the build positions (before this step's move)
+    if (ng > 0) {
+        slab_ghost_table<<<cdiv(ng, kThreads), kThreads, 0, st>>>(nt, lo, no, C.uid, S.g_uid, S.g_idx);
+        size_t tb = S.sort_tmp_bytes;
+        CUDA_TRY(c, cub::DeviceRadixSort::SortPairs(S.sort_tmp, tb, S.g_uid, S.g_uid_sorted, S.g_idx, S.g_idx_sorted,
+                                                    ng, 0, 64, st));
+    }
+    CUDA_TRY(c, cudaMemsetAsync(S.counts, 0, sizeof(unsigned long long) * kHist, st));
+    if (no > 0)
+        slab_refresh_lists<T, false><<<cdiv(no, kThreads), kThreads, 0, st>>>(no, lo, S.g, S.B, C.rec, S.counts,
+                                                                              nullptr, nullptr, nullptr);
+    unsigned long long h[kHist];
+    CUDA_TRY(c, cudaMemcpyAsync(h, S.counts, sizeof(unsigned long long) * 3 * W, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    unsigned long long off[kHist], acc = 0;
+    for (int k = 0; k < 3 * W; ++k) {
+        off[k] = acc;
+        S.ref_counts[k] = (int64_t)h[k];
+        acc += h[k];
+    }
+    S.ref_total = (int64_t)acc;
+    if (acc > 0) {
+        CUDA_TRY(c, cudaMemcpyAsync(S.ref_off, off, sizeof(unsigned long long) * 3 * W, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(c, cudaMemsetAsync(S.cursor, 0, sizeof(unsigned) * kHist, st));
+        slab_refresh_lists<T, true><<<cdiv(no, kThreads), kThreads, 0, st>>>(no, lo, S.g, S.B, C.rec, nullptr,
+                                                                             S.ref_off, S.cursor, S.ref_list);
+    }
+    LAUNCH_CHECK(c);
+    c->launches += 3;
+    S.n_total = nt;
+    S.rot_build = lo;
+    S.x_lo_abs = S.g.ox + (double)S.x0 * S.g.L;
+    S.x_hi_abs = S.g.ox + (double)S.x1 * S.g.L;
+    S.refresh_ready = true;
+    return CG_OK;
+}
+
+// a list step on a slab: grid counts over owned + ghosts, list sweep of the
+// owned agents (indices [rot, rot + n_owned), buffers at index - rot)
+template <typename T>
+static int slab_list_step(cg_context *c, const double params[5], bool freeze, bool record)
+{
+    auto &S = c->slab;
+    const int slot = (int)(c->steps_done % kRing);
+    cudaStream_t st = c->stream;
+    const int rot = S.rot_build, nt = (int)S.n_total, no = (int)c->n_owned;
+    // sub-grid: every present agent lies within 3 box lengths (+ the motion
+    // since the rebuild) of the owned slab's x range at the rebuild
+    Geometry g = S.g;
+    const auto plane = [&](double x) {
+        return (int)std::min<double>(std::max<double>(std::floor((x - S.g.ox) / S.g.L), 0.0), S.g.dimx - 1.0);
+    };
+    const int xl = plane(S.x_lo_abs - 4.0 * S.g.L), xh = plane(S.x_hi_abs + 4.0 * S.g.L) + 1;
+    g.xoff = xl;
+    g.gdimx = S.g.dimx;
+    g.dimx = std::max(xh - xl, 1);
+    g.nb = g.dimx * g.dimy * g.dimz;
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][0], st));
+    int rc;
+    if ((rc = ensure_boxes(c, g.nb))) return rc;
+    c->geo = g;
+    c->bd = make_decode(g);
+    unsigned long long *stat = c->stat_dev + slot * kStatSlots;
+    CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
+    const int cp = c->cur_pos, ca = c->cur_attr;
+    box_keys<T><<<cdiv(nt, kThreads), kThreads, 0, st>>>(nt, g, 1.0 / g.L, (const Rec<T> *)c->b.rec[cp] - rot,
+                                                         c->count, c->b.key_rank);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
+    ListArgs<T> A{};
+    A.n = no;
+    A.own_lo = rot;
+    A.g = g;
+    A.bd = c->bd;
+    A.key_rank = c->b.key_rank;
+    A.off = c->offset;
+    A.rec = (const Rec<T> *)c->b.rec[cp] - rot;
+    A.adh = (const T *)c->b.adh[ca] - rot;
+    A.uid = c->b.uid[ca] - rot;
+    A.p = make_params<T>(params);
+    A.nbr = c->nbr;
+    A.nbr_n = c->nbr_n;
+    A.nbr_stride = c->nbr_cap;
+    A.disp_x = (T *)c->b.disp[0] - rot;
+    A.disp_y = (T *)c->b.disp[1] - rot;
+    A.disp_z = (T *)c->b.disp[2] - rot;
+    A.new_rec = freeze ? nullptr : (Rec<T> *)c->b.rec[1 - cp] - rot;
+    A.rec_m = record ? c->b.rec_m - rot : nullptr;
+    A.rec_nk = record ? c->b.rec_nk - rot : nullptr;
+    A.pkey = nullptr;
+    A.slots = c->slots;
+    bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
+    if (no > 0) {
+        list_sweep_kernel<T><<<cdiv(no, kThreads), kThreads, 0, st>>>(A);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+    }
+    finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, stat, c->bbox_dev,
+                                         FINISH_COUNTERS | (freeze ? 0 : FINISH_BBOX));
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    if (!freeze)
+        CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    c->bbox_valid = true;
+    c->relaid = false;
+    c->last_dense = false;
+    c->list_life++;
+    c->list_steps++;
+    return CG_OK;
+}
+
 template <typename T>
 static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t *step_id)
 {
     auto &S = c->slab;
     if (!S.planned || !S.packed) return fail(c, CG_ERR_STATE, "cg_slab_step without cg_slab_plan / cg_slab_pack");
-    c->list_valid = false;
-    c->last_kind = 0;
     const int slot = (int)(c->steps_done % kRing);
     cg_step_stats &St = c->ring[slot];
     std::memset(&St, 0, sizeof St);
@@ -1122,33 +1388,57 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
     *step_id = c->steps_done;
     cudaStream_t st = c->stream;
     int rc;
-    // exact bbox of the owned set (the sweep's shell filter needs it)
-    if (!c->bbox_valid && c->n_owned > 0 && (rc = standalone_bbox<T>(c))) return rc;
-    // sub-grid: global planes [x0 - 1, x1 + 1) clipped to the grid
-    Geometry g = S.g;
-    const int xl = std::max(S.x0 - 1, 0), xh = std::min(S.x1 + 1, S.g.dimx);
-    g.xoff = xl;
-    g.gdimx = S.g.dimx;
-    g.dimx = std::max(xh - xl, 1);
-    g.nb = g.dimx * g.dimy * g.dimz;
     const bool freeze = (flags & CG_STEP_FREEZE) != 0;
     const bool record = (flags & CG_STEP_RECORD) != 0;
-    if (c->n > 0) {
-        // relaid storage as in the single-context step; the owned planes are
-        // the middle slot range, rotated to the front by the lo-ghost count
-        // (the first slot of local plane 1 when a lo ghost plane exists)
-        const bool relayout = c->sweep_impl == 1 && c->n > 1 && (S.steps % c->relayout_every == 0);
-        const int rot = xl == S.x0 - 1 ? (int)S.ghost_lo : 0;
-        if ((rc = build_grid_geo<T>(c, g, relayout && rot <= c->b.head, false, rot))) return rc;
-        S.steps++;
-        CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
-        if ((rc = run_sweep<T>(c, params, freeze, record))) return rc;
+    if (S.list_mode) {
+        if ((rc = slab_list_step<T>(c, params, freeze, record))) return rc;
         if (!freeze) c->cur_pos = 1 - c->cur_pos;
+        c->last_kind = 2;
+        St.sweep_kind = 2;
     } else {
-        CUDA_TRY(c, cudaMemsetAsync(c->stat_dev + slot * kStatSlots, 0, sizeof(unsigned long long) * kStatSlots, st));
-        for (int e = 0; e < 3; ++e) CUDA_TRY(c, cudaEventRecord(c->ev[slot][e], st));
-        c->bbox_valid = false;
+        c->list_valid = false;
+        // exact bbox of the owned set (the sweep's shell filter needs it)
+        if (!c->bbox_valid && c->n_owned > 0 && (rc = standalone_bbox<T>(c))) return rc;
+        // sub-grid: global planes [x0 - band, x1 + band) clipped to the grid
+        Geometry g = S.g;
+        const int xl = std::max(S.x0 - S.B.band, 0), xh = std::min(S.x1 + S.B.band, S.g.dimx);
+        g.xoff = xl;
+        g.gdimx = S.g.dimx;
+        g.dimx = std::max(xh - xl, 1);
+        g.nb = g.dimx * g.dimy * g.dimz;
+        bool build = false;
+        if (c->n > 0) {
+            // relaid storage as in the single-context step; the owned planes are
+            // the middle slot range, rotated to the front by the lo-ghost count
+            const bool relayout = c->sweep_impl == 1 && c->n > 1 && (S.steps % c->relayout_every == 0);
+            const int rot = (int)S.ghost_lo;
+            if ((rc = build_grid_geo<T>(c, g, relayout && rot <= c->b.head, false, rot))) return rc;
+            S.steps++;
+            CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
+            build = S.B.band == 3 && c->list_wait == 0 && !c->last_dense;
+            if (c->list_wait > 0) c->list_wait--;
+            if (build) {
+                if ((rc = ensure_lists(c))) return rc;
+                c->list_skin_used = c->list_skin < 0 ? 0.07 * S.g.L : c->list_skin;
+                build = c->list_skin_used > 0 && c->list_skin_used <= S.g.L;
+            }
+            if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
+            if (build) {
+                if ((rc = slab_list_tables<T>(c))) return rc;
+                c->list_builds++;
+            }
+            if (!freeze) c->cur_pos = 1 - c->cur_pos;
+        } else {
+            CUDA_TRY(c, cudaMemsetAsync(c->stat_dev + slot * kStatSlots, 0, sizeof(unsigned long long) * kStatSlots,
+                                        st));
+            for (int e = 0; e < 3; ++e) CUDA_TRY(c, cudaEventRecord(c->ev[slot][e], st));
+            c->bbox_valid = false;
+        }
+        if (!build) c->n = c->n_owned;   // this step's ghosts are dropped (list steps keep them)
+        c->last_kind = build ? 1 : 0;
+        St.sweep_kind = build ? 1 : 0;
     }
+    c->last_freeze = freeze;
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][3], st));
     CUDA_TRY(c, cudaMemcpyAsync(c->stat_host + slot * kStatSlots, c->stat_dev + slot * kStatSlots,
                                 sizeof(unsigned long long) * kStatSlots, cudaMemcpyDeviceToHost, st));
@@ -1160,7 +1450,6 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
     St.origin[1] = S.g.oy;
     St.origin[2] = S.g.oz;
     St.box_length = S.g.L;
-    c->n = c->n_owned;   // this step's ghosts are dropped
     c->last_record = record;
     c->have_grid = false;   // the sub-grid is not exportable
     c->pres_state = PRES_IDENTITY;
@@ -1259,7 +1548,7 @@ const char *cg_last_error(const cg_context *c) { return c ? c->err.c_str() : "nu
 
 void *cg_stream(cg_context *c) { return c ? (void *)c->stream : nullptr; }
 
-int64_t cg_count(const cg_context *c) { return c ? c->n : -1; }
+int64_t cg_count(const cg_context *c) { return c ? c->n_owned : -1; }   // agents owned (a slab also holds ghosts)
 
 int64_t cg_launch_count(const cg_context *c) { return c ? c->launches : -1; }
 
@@ -1378,7 +1667,7 @@ int cg_download(cg_context *c, void *px, void *py, void *pz, void *diameter, voi
 {
     if (!c) return CG_ERR_VALUE;
     CUDA_TRY(c, cudaSetDevice(c->device));
-    const int64_t n = c->n;
+    const int64_t n = c->n_owned;   // a slab keeps its ghosts after the owned agents
     if (n == 0) return CG_OK;
     int rc = materialize_presentation(c);
     if (rc) return rc;
@@ -1668,7 +1957,7 @@ int cg_reserve(cg_context *c, int64_t capacity)
     return CG_OK;
 }
 
-int cg_local_bbox(cg_context *c, double out[7])
+int cg_local_bbox(cg_context *c, double out[9])
 {
     if (!c) return CG_ERR_VALUE;
     CUDA_TRY(c, cudaSetDevice(c->device));
@@ -1676,6 +1965,7 @@ int cg_local_bbox(cg_context *c, double out[7])
         out[0] = out[1] = out[2] = INFINITY;
         out[3] = out[4] = out[5] = -INFINITY;
         out[6] = c->max_diam;
+        out[7] = out[8] = 0.0;
         return CG_OK;
     }
     int rc = CG_OK;
@@ -1686,16 +1976,20 @@ int cg_local_bbox(cg_context *c, double out[7])
     if (rc) return rc;
     for (int k = 0; k < 6; ++k) out[k] = c->bbox_host[k];
     out[6] = c->max_diam;
+    // the last step's largest squared displacement and neighbour-list
+    // overflows (all-reduced with the bbox for the list decision)
+    out[7] = c->last_kind != 0 && !c->last_freeze ? c->bbox_host[7] : 0.0;
+    out[8] = c->last_kind == 1 ? c->bbox_host[8] : 0.0;
     return CG_OK;
 }
 
-int cg_slab_plan(cg_context *c, const double bbox[7], double interaction_radius, int64_t box_cap, int world,
+int cg_slab_plan(cg_context *c, const double bbox[9], double interaction_radius, int64_t box_cap, int world,
                  int rank, int64_t *counts, int64_t planes[2])
 {
     if (!c) return CG_ERR_VALUE;
     if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world) return fail(c, CG_ERR_VALUE, "bad world/rank");
     CUDA_TRY(c, cudaSetDevice(c->device));
-    if (c->n != c->n_owned) return fail(c, CG_ERR_STATE, "ghosts from an unfinished slab step");
+    if (c->slab.planned) return fail(c, CG_ERR_STATE, "cg_slab_plan twice without cg_slab_step");
     return c->prec == CG_FP64 ? slab_plan_t<double>(c, bbox, interaction_radius, box_cap, world, rank, counts, planes)
                               : slab_plan_t<float>(c, bbox, interaction_radius, box_cap, world, rank, counts, planes);
 }
@@ -1713,7 +2007,7 @@ int cg_slab_unpack(cg_context *c, const void *recv, const int64_t *recv_counts)
     if (!c || !recv_counts) return CG_ERR_VALUE;
     CUDA_TRY(c, cudaSetDevice(c->device));
     if (!c->slab.packed) return fail(c, CG_ERR_STATE, "cg_slab_unpack without cg_slab_pack");
-    if (c->n != c->n_owned) return fail(c, CG_ERR_STATE, "cg_slab_unpack called twice");
+    if (c->slab.unpacked) return fail(c, CG_ERR_STATE, "cg_slab_unpack called twice");
     return c->prec == CG_FP64 ? slab_unpack_t<double>(c, recv, recv_counts)
                               : slab_unpack_t<float>(c, recv, recv_counts);
 }

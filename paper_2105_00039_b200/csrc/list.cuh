@@ -23,7 +23,8 @@ namespace cg {
 
 template <typename T>
 struct ListArgs {
-    int n;
+    int n;                    // agents swept: indices [own_lo, own_lo + n)
+    int own_lo;               // 0 on a single context; the lo-ghost count on a slab
     Geometry g;
     BoxDecode bd;
     const int2 *key_rank;     // this step's box of every storage index
@@ -66,10 +67,11 @@ __device__ __noinline__ void degenerate_pair(uint64_t ui, uint64_t uj, T mag, T 
 template <typename T>
 __global__ void __launch_bounds__(kThreads, CG_LIST_MINB) list_sweep_kernel(ListArgs<T> A)
 {
-    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int a = A.own_lo + t;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
     float dmax2 = 0.f;
-    if (a < A.n) {
+    if (t < A.n) {
         const int key = A.key_rank[a].x;
         if (A.pkey) A.pkey[a] = key;
         int ix, iy, iz;

@@ -39,6 +39,7 @@ constexpr int kMaxWorld = 64;
 
 struct SlabBounds {
     int world;
+    int band;               // ghost planes on each side of a slab (1; 3 with neighbour lists)
     int x[kMaxWorld + 1];   // plane bounds X_0 .. X_world
 };
 
@@ -49,8 +50,17 @@ __device__ __forceinline__ int slab_owner(const SlabBounds &B, int ix)
     return r;
 }
 
-// dest byte: owner rank (6 bits) | 0x40 ghost of owner+1 | 0x80 ghost of owner-1
-constexpr unsigned char kGhostUp = 0x40, kGhostDown = 0x80;
+// f(q', kind) for every other rank q' whose ghost band holds plane ix (owned
+// by q): kind 1 = within band planes below q''s slab, 2 = above it
+template <typename F>
+__device__ __forceinline__ void for_each_ghost_dest(const SlabBounds &B, int ix, int q, F &&f)
+{
+    for (int r = q + 1; r < B.world && B.x[r] - B.band <= ix; ++r) f(r, 1);
+    for (int r = q - 1; r >= 0 && B.x[r + 1] + B.band > ix; --r) f(r, 2);
+}
+
+// dest byte: owner rank (6 bits) | 0x40 ghost of some other rank
+constexpr unsigned char kGhostAny = 0x40;
 
 // hist layout (kHist entries): [3q + 0] migrants to q (q != rank), [3q + 1]
 // lo ghosts of q, [3q + 2] hi ghosts of q, [3 world] agents that stay
@@ -72,15 +82,16 @@ __global__ void __launch_bounds__(kThreads) slab_dest(int n, Geometry g, SlabBou
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int ix = axis_box((double)rec[i].x, g.ox, g.L, g.gdimx);
         const int q = slab_owner(B, ix);
-        const bool up = q + 1 < W && ix == B.x[q + 1] - 1;   // in the lo ghost plane of q + 1
-        const bool down = q > 0 && ix == B.x[q];               // in the hi ghost plane of q - 1
-        dest[i] = (unsigned char)(q | (up ? kGhostUp : 0) | (down ? kGhostDown : 0));
+        bool ghost = false;
+        for_each_ghost_dest(B, ix, q, [&](int r, int kind) {
+            atomicAdd(hist + 3 * r + kind, 1u);
+            ghost = true;
+        });
+        dest[i] = (unsigned char)(q | (ghost ? kGhostAny : 0));
         const unsigned act = __activemask();
         const int bin = q == rank ? 3 * W : 3 * q;
         const unsigned peers = __match_any_sync(act, bin);
         if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + bin, (unsigned)__popc(peers));
-        if (up) atomicAdd(hist + 3 * (q + 1) + 1, 1u);
-        if (down) atomicAdd(hist + 3 * (q - 1) + 2, 1u);
     }
     __syncthreads();
     for (int k = threadIdx.x; k <= 3 * W; k += blockDim.x)
@@ -111,7 +122,7 @@ __global__ void slab_lists(int n, int n_keep, int rank, const unsigned char *__r
     if (i >= n) return;
     const unsigned char d = dest[i];
     const bool leaving = (d & 63) != rank;
-    warp_append(leaving || (d & (kGhostUp | kGhostDown)), cnt + 0, out, i);
+    warp_append(leaving || (d & kGhostAny), cnt + 0, out, i);
     warp_append(leaving && i < n_keep, cnt + 1, holes, i);
     warp_append(!leaving && i >= n_keep, cnt + 2, movers, i);
 }
@@ -151,7 +162,7 @@ __device__ __forceinline__ void store_record(const SlabCols<T> &C, int i, const 
 // (kind 0 migrant, 1 lo ghost of q, 2 hi ghost of q); order within a run is
 // arbitrary (the step's results do not depend on storage order)
 template <typename T>
-__global__ void slab_pack_out(int nout, int rank, const int *__restrict__ out_list,
+__global__ void slab_pack_out(int nout, int rank, Geometry g, SlabBounds B, const int *__restrict__ out_list,
                               const unsigned char *__restrict__ dest, const unsigned long long *__restrict__ seg_off,
                               unsigned *__restrict__ cursor, SlabCols<T> C, SlabRecord<T> *__restrict__ out)
 {
@@ -163,8 +174,12 @@ __global__ void slab_pack_out(int nout, int rank, const int *__restrict__ out_li
     SlabRecord<T> rec;
     load_record(C, i, rec);
     if (q != rank) out[seg_off[3 * q] + atomicAdd(cursor + 3 * q, 1u)] = rec;
-    if (d & kGhostUp) out[seg_off[3 * (q + 1) + 1] + atomicAdd(cursor + 3 * (q + 1) + 1, 1u)] = rec;
-    if (d & kGhostDown) out[seg_off[3 * (q - 1) + 2] + atomicAdd(cursor + 3 * (q - 1) + 2, 1u)] = rec;
+    if (d & kGhostAny) {
+        const int ix = axis_box((double)rec.v[0], g.ox, g.L, g.gdimx);
+        for_each_ghost_dest(B, ix, q, [&](int r, int kind) {
+            out[seg_off[3 * r + kind] + atomicAdd(cursor + 3 * r + kind, 1u)] = rec;
+        });
+    }
 }
 
 template <typename T>
@@ -194,6 +209,89 @@ __global__ void slab_unpack_segs(int total, SlabSegs S, const SlabRecord<T> *__r
     int s = 0;
     while (S.start[s + 1] <= k) ++s;
     store_record(C, S.dst[s] + (int)(k - S.start[s]), in[k]);
+}
+
+
+// ------------------------------------------------------------ neighbour lists across slabs
+// Between list rebuilds the partition is frozen: every rank keeps its owned
+// agents and the ghost set it received at the rebuild (a band of 3 planes on
+// each side, so every agent that can enter an owned agent's 27 boxes before
+// the next rebuild is present), and each step the owners refresh the ghosts'
+// records.  Indices are the build step's (relaid) indices; the buffers are
+// addressed at index - rot (lo ghosts in the front headroom).
+
+// ghost table: the ghost indices [0, lo) U [lo + n_owned, n_total) with their
+// uids (sorted afterwards, so refresh records can be matched by uid)
+__global__ void slab_ghost_table(int n_total, int lo, int n_owned, const uint64_t *__restrict__ uid,
+                                 uint64_t *__restrict__ g_uid, int *__restrict__ g_idx)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ng = n_total - n_owned;
+    if (k >= ng) return;
+    const int i = k < lo ? k : k + n_owned;
+    g_uid[k] = uid[i];
+    g_idx[k] = i;
+}
+
+// refresh lists: owned agents in another rank's ghost band (at the build
+// positions), pass 0 counts per (rank, kind) bin, pass 1 fills the runs
+template <typename T, bool FILL>
+__global__ void slab_refresh_lists(int n_owned, int lo, Geometry g, SlabBounds B, const Rec<T> *__restrict__ rec,
+                                   unsigned long long *__restrict__ counts, const unsigned long long *__restrict__ run_off,
+                                   unsigned *__restrict__ cursor, int *__restrict__ list)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_owned) return;
+    const int i = lo + k;
+    const int ix = axis_box((double)rec[i].x, g.ox, g.L, g.gdimx);
+    const int q = slab_owner(B, ix);
+    for_each_ghost_dest(B, ix, q, [&](int r, int kind) {
+        const int bin = 3 * r + kind;
+        if (FILL) list[run_off[bin] + atomicAdd(cursor + bin, 1u)] = i;
+        else atomicAdd(counts + bin, 1ull);
+    });
+}
+
+template <typename T>
+__global__ void slab_refresh_pack(int count, const int *__restrict__ list, SlabCols<T> C,
+                                  SlabRecord<T> *__restrict__ out)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    SlabRecord<T> r;
+    load_record(C, list[k], r);
+    out[k] = r;
+}
+
+__global__ void slab_recv_keys(int count, const unsigned char *__restrict__ recv, int rec_bytes, int uid_off,
+                               uint64_t *__restrict__ keys, int *__restrict__ vals)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    keys[k] = *reinterpret_cast<const uint64_t *>(recv + (size_t)k * rec_bytes + uid_off);
+    vals[k] = k;
+}
+
+// the p-th received record (by uid) refreshes the p-th ghost (by uid)
+template <typename T>
+__global__ void slab_refresh_scatter(int count, const SlabRecord<T> *__restrict__ in, const int *__restrict__ order,
+                                     const uint64_t *__restrict__ got_uid, const uint64_t *__restrict__ want_uid,
+                                     const int *__restrict__ g_idx, Rec<T> *__restrict__ rec,
+                                     unsigned *__restrict__ mismatch)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= count) return;
+    if (got_uid[p] != want_uid[p]) {
+        atomicAdd(mismatch, 1u);
+        return;
+    }
+    const SlabRecord<T> r = in[order[p]];
+    Rec<T> v;
+    v.x = r.v[0];
+    v.y = r.v[1];
+    v.z = r.v[2];
+    v.d = r.v[3];
+    rec[g_idx[p]] = v;
 }
 
 }  // namespace cg

@@ -31,7 +31,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, steps, params5, summation, out_q):
+def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -45,6 +45,7 @@ def _worker(rank, world, port, steps, params5, summation, out_q):
     mine = (full.uid % world) == rank            # ignores the slab rule: step 1 migrates
     ctx = _native.Context(0, full.dtype)
     ctx.set_option(_native.CG_OPT_SUMMATION, summation)
+    ctx.set_option(_native.CG_OPT_LIST_SKIN, skin)
     ctx.reserve(full.count)
     ctx.upload(full.position_x[mine], full.position_y[mine], full.position_z[mine],
                full.diameter[mine], full.adherence[mine], full.uid[mine])
@@ -52,21 +53,27 @@ def _worker(rank, world, port, steps, params5, summation, out_q):
     stats = [runner.step(params5) for _ in range(steps)]
     cols = ctx.download()
     out_q.put((rank, cols, [(s.force_evals, s.candidates, s.degenerate_pairs,
-                             s.migrated_in + s.migrated_out, s.ghosts) for s in stats]))
+                             s.migrated_in + s.migrated_out, s.ghosts) for s in stats], ctx.list_stats()))
     ctx.close()
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,summation", [(2, 0), (3, 1)])
-def test_slab_ranks_match_single_context(cuda_required, world, summation):
+@pytest.mark.parametrize("world,summation,skin,params", [
+    (2, 0, 0, (2.0, 1.0, 0.01, 3.0, 1.0)), (3, 1, 0, (2.0, 1.0, 0.01, 3.0, 1.0)),
+    (2, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)), (3, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0))])
+def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, params):
+    """skin 0: a full exchange every step; skin -1: neighbour lists, the
+    partition frozen and the ghosts refreshed between rebuilds (small
+    timestep: the lists serve several steps)."""
     import multiprocessing as mp
     from paper_2105_00039_b200 import _native
-    steps = 4
+    PARAMS5 = np.array(params)
+    steps = 4 if skin == 0 else 9
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
     port = _free_port()
-    procs = [mpc.Process(target=_worker, args=(r, world, port, steps, PARAMS5, summation, q))
+    procs = [mpc.Process(target=_worker, args=(r, world, port, steps, PARAMS5, summation, q, skin))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -98,3 +105,5 @@ def test_slab_ranks_match_single_context(cuda_required, world, summation):
         assert all(r[2][k][:3] == ref_counters[k] for r in res)
     assert sum(r[2][0][3] for r in res) > 0          # agents migrated
     assert all(r[2][0][4] > 0 for r in res)          # ghosts were exchanged
+    if skin != 0:                                    # list steps ran on every rank
+        assert all(r[3]["list_steps"] > 0 and r[3]["builds"] > 0 for r in res), [r[3] for r in res]
