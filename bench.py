@@ -157,6 +157,22 @@ def profiled_traffic(config, precision, kernel):
         return None
 
 
+def fp64_view(cands, evals, ms):
+    """Secondary roofline (diagnostic): the reference's cost model
+    F = 11 flops per stencil candidate + 14 per kept pair (mechanics.py:34-40)
+    per step, against the measured FP64 DFMA rate (profiles/r1_fp64_peak.json,
+    tools/fp64_peak.cu)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_fp64_peak.json")) as fh:
+            peak = float(json.load(fh)["dfma_tflops"])
+    except (OSError, KeyError, ValueError):
+        return None
+    flops = 11.0 * cands + 14.0 * evals
+    achieved = flops / (ms * 1e-3) / 1e12
+    return {"alg_gflop_per_step": flops / 1e9, "achieved_tflops": achieved, "peak_tflops": peak,
+            "frac": achieved / peak, "peak_source": "measured DFMA (profiles/r1_fp64_peak.json)"}
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -457,6 +473,7 @@ def main():
                      "kernel": kernel_name, "alg_bytes_per_agent": bal,
                      "kernel_ms": t_force, "peak_source": peak_src, "sweep_mix": sweep_mix},
         "step_roofline_frac": n * bal / (ms * 1e-3) / 1e9 / peak,
+        "fp64_view": fp64_view(cands, evals, ms),
         "pair_interactions_per_s": evals * world / (ms * 1e-3),
         "candidates_per_s": cands * world / (ms * 1e-3),
         "gpu_launches": launches,
