@@ -1,5 +1,7 @@
 """Per-config device timings for BASELINE.json's configurations (C1-C4), fp64
-and fp32, C3 with and without the Z-order sort; one JSON line per run.
+and fp32, C3 with and without the Z-order sort; one JSON line per run (mean
+over 12 steps after 3 warm-up steps; step kinds 0 grid sweep, 1 list build,
+2 list sweep).
 
 usage: python tools/configs.py [names...]   names: c1 c2 c2f c4 c4f c3_<d> c3_<d>_nosort
 """
@@ -15,7 +17,7 @@ from paper_2105_00039_b200 import _native as N, workloads  # noqa: E402
 from paper_2105_00039_b200.pool import PrecisionMode  # noqa: E402
 
 
-def run(name, steps=5, warm=3):
+def run(name, steps=12, warm=3):
     prec = PrecisionMode.FP32 if name.endswith("f") else PrecisionMode.FP64
     base = name.rstrip("f")
     nosort = base.endswith("_nosort")
@@ -38,10 +40,13 @@ def run(name, steps=5, warm=3):
     for _ in range(warm):
         ctx.step(params, None, 1 << 24, flags)
     sts = [ctx.step(params, None, 1 << 24, flags) for _ in range(steps)]
-    tot = float(np.median([s.t_total_ms for s in sts]))
+    tot = float(np.mean([s.t_total_ms for s in sts]))
     st = sts[-1]
+    kinds = [int(s.sweep_kind) for s in sts]
     out = {"config": name, "agents": pool.count, "dtype": str(np.dtype(pool.dtype)), "sort": not nosort,
-           "ms_total": tot, "ms_grid": st.t_grid_ms, "ms_sort": st.t_sort_ms, "ms_force": st.t_force_ms,
+           "ms_total": tot, "ms_total_median": float(np.median([s.t_total_ms for s in sts])),
+           "step_kinds": {k: kinds.count(k) for k in sorted(set(kinds))},
+           "ms_grid": st.t_grid_ms, "ms_sort": st.t_sort_ms, "ms_force": st.t_force_ms,
            "agent_updates_per_s": pool.count / (tot * 1e-3),
            "pair_interactions_per_s": st.force_evals / (tot * 1e-3),
            "evals_per_agent": st.force_evals / pool.count, "cands_per_agent": st.candidates / pool.count,
