@@ -106,3 +106,22 @@ def test_lists_match_oracle(cuda_required):
             assert np.array_equal(cols[a], getattr(ref, b)), (k, a)
     assert ctx.list_stats()["list_steps"] >= 3
     ctx.close()
+
+
+def test_list_overflow_falls_back(cuda_required):
+    """A sparse pool with one crowded spot (more than 48 partners within the
+    skin for some agents): the build reports the overflow, the lists are not
+    used, and every step still matches the list-free run bit for bit."""
+    from paper_2105_00039_b200.pool import AgentPool
+    from paper_2105_00039_b200.workloads import jittered_lattice_positions
+    pos = jittered_lattice_positions(20, 8.0, 1.0, 4)
+    rng = np.random.default_rng(9)
+    pos[:80] = 80.0 + rng.uniform(-4.0, 4.0, (80, 3))     # 80 agents inside one box
+    pool = AgentPool.from_arrays(pos, 10.0, 0.4)
+    got, st = _run(pool, -1, 12, 0)
+    ref, _ = _run(pool, 0, 12, 0)
+    assert st["builds"] >= 1 and st["list_steps"] == 0, st
+    for a, b in zip(got, ref):
+        assert a[0] == b[0]
+        for col in a[1]:
+            assert np.array_equal(a[1][col], b[1][col])
