@@ -273,13 +273,15 @@ def main_slab(args, rank, world, local):
     ctx.reserve(int(n0 * 1.05) + 4 * 256 * 256 * 2 + 4096)
     ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
     ex = TorchExchange(device="cuda", device_buffers=args.exchange == "nccl")
-    runner = SlabRunner(ctx, ex)
+    # counters all-reduced once for the timed steps (inside the timed region)
+    runner = SlabRunner(ctx, ex, sync_counters=False)
     params = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
     flags = _native.CG_STEP_FREEZE if args.freeze else 0
     stream = torch.cuda.ExternalStream(ctx.stream)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             runner.step(params, flags)
+        runner.collect()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         launches0 = ctx.launches
@@ -287,7 +289,9 @@ def main_slab(args, rank, world, local):
         torch.cuda.synchronize()
         with Clocks(local) as clk:
             ev0.record(stream)
-            stats = [runner.step(params, flags) for _ in range(args.steps)]
+            for _ in range(args.steps):
+                runner.step(params, flags)
+            stats = runner.collect()
             ev1.record(stream)
             torch.cuda.synchronize()
         launches = ctx.launches - launches0
@@ -323,6 +327,7 @@ def main_slab(args, rank, world, local):
                 n = ctx.n
                 ctx.download(into={k: v[:n] for k, v in pin.items()})
                 d2h += n * (8 * np.dtype(pool.dtype).itemsize + 8)
+            runner.collect()
         torch.cuda.synchronize()
         t_e2e = reduce_max((_t.perf_counter() - t0) / args.e2e_steps, world)
         e2e = {"value": total / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.e2e_steps,

@@ -166,8 +166,10 @@ int64_t cg_record_bytes(const cg_context *ctx);
 /* Pre-size the agent buffers (before cg_upload) for arrivals and ghosts. */
 int cg_reserve(cg_context *ctx, int64_t capacity);
 /* Exact bbox of the owned agents (min xyz, max xyz), max diameter, the last
- * step's largest squared displacement and neighbour-list overflow count: all
- * nine are all-reduced with MAX (after negating the three minima). */
+ * step's largest squared displacement, and a neighbour-list veto (the build's
+ * overflow count, or 1 when this rank neither built lists nor ran a list step
+ * last): all nine are all-reduced with MAX (after negating the three minima),
+ * so every rank takes the same list decision in cg_slab_plan. */
 int cg_local_bbox(cg_context *ctx, double out[9]);
 /* Geometry from the global bbox (spatial.py:99-116; GridOverflowError as
  * cg_step) and slab planes: planes = {X_rank, X_rank+1}.  counts (3 * world):
@@ -190,6 +192,11 @@ int cg_slab_pack(cg_context *ctx, void *send);
 int cg_slab_unpack(cg_context *ctx, const void *recv, const int64_t *recv_counts);
 /* The mechanical step on the owned agents over the slab's sub-grid. */
 int cg_slab_step(cg_context *ctx, const double params[5], int flags, cg_step_stats *stats);
+/* After cg_slab_plan: -1 for a rebuild step, else the id of the list epoch
+ * (constant between rebuilds): a refresh step whose run sizes -- sent and
+ * received -- are those of the previous refresh step of the same epoch, so a
+ * caller may skip the counts all-to-all. */
+int64_t cg_slab_list_epoch(const cg_context *ctx);
 
 #ifdef __cplusplus
 }

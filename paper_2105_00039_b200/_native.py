@@ -31,7 +31,7 @@ EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_
             "cg_host_alloc", "cg_host_free", "cg_record_bytes", "cg_reserve", "cg_local_bbox",
             "cg_slab_plan", "cg_slab_pack", "cg_slab_unpack",
             "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill",
-            "cg_list_stats")
+            "cg_list_stats", "cg_slab_list_epoch")
 
 
 class GridOverflowError(RuntimeError):
@@ -100,6 +100,7 @@ def load():
         "cg_force_phase": ([_P, _I64] + [_P] * 7 + [_I64] * 3 + [_P] * 5, ctypes.c_int),
         "cg_neighbor_counts": ([_P, ctypes.c_double, _P], ctypes.c_int),
         "cg_list_stats": ([_P, _P], ctypes.c_int),
+        "cg_slab_list_epoch": ([_P], _I64),
         "cg_neighbor_fill": ([_P, ctypes.c_double, _P, _P], ctypes.c_int),
         "cg_record_bytes": ([_P], _I64),
         "cg_reserve": ([_P, _I64], ctypes.c_int),
@@ -275,6 +276,10 @@ class Context:
         check(load().cg_slab_plan(self.h, ptr(bb), ir, int(box_cap), int(world), int(rank),
                                   ptr(counts), ptr(planes)), self.h)
         return counts, planes
+
+    def slab_list_epoch(self):
+        """-1 for a rebuild step, else the list epoch of the planned refresh step."""
+        return int(load().cg_slab_list_epoch(self.h))
 
     def slab_pack(self, send_ptr):
         check(load().cg_slab_pack(self.h, send_ptr), self.h)

@@ -1965,7 +1965,8 @@ int cg_local_bbox(cg_context *c, double out[9])
         out[0] = out[1] = out[2] = INFINITY;
         out[3] = out[4] = out[5] = -INFINITY;
         out[6] = c->max_diam;
-        out[7] = out[8] = 0.0;
+        out[7] = 0.0;
+        out[8] = c->last_kind == 2 ? 0.0 : 1.0;   // no lists of its own: veto list steps
         return CG_OK;
     }
     int rc = CG_OK;
@@ -1979,7 +1980,9 @@ int cg_local_bbox(cg_context *c, double out[9])
     // the last step's largest squared displacement and neighbour-list
     // overflows (all-reduced with the bbox for the list decision)
     out[7] = c->last_kind != 0 && !c->last_freeze ? c->bbox_host[7] : 0.0;
-    out[8] = c->last_kind == 1 ? c->bbox_host[8] : 0.0;
+    // list veto: overflows of a build, or 1 when this rank neither built lists
+    // nor ran a list step last (every rank must take the same decision)
+    out[8] = c->last_kind == 1 ? c->bbox_host[8] : (c->last_kind == 2 ? 0.0 : 1.0);
     return CG_OK;
 }
 
@@ -2091,6 +2094,12 @@ static int neighbor_check(cg_context *c, double radius)
 }
 
 extern "C" {
+
+int64_t cg_slab_list_epoch(const cg_context *c)
+{
+    if (!c) return -1;
+    return c->slab.planned && c->slab.list_mode ? c->list_builds : -1;
+}
 
 int cg_list_stats(cg_context *c, int64_t out[4])
 {

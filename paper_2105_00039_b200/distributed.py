@@ -113,18 +113,30 @@ class SlabStats:
 
 class SlabRunner:
     """Drives cg_slab_* on one rank.  ``ctx`` is a _native.Context (or any
-    object with the same slab methods, e.g. the CPU mock in tests/)."""
+    object with the same slab methods, e.g. the CPU mock in tests/).
 
-    def __init__(self, ctx, exchange):
+    ``sync_counters=False`` defers the counter all-reduce: ``step`` returns
+    this rank's counters and ``collect()`` all-reduces every pending step's
+    counters in one collective (one host round trip per step fewer)."""
+
+    def __init__(self, ctx, exchange, sync_counters=True):
         self.ctx, self.ex = ctx, exchange
         self.rank, self.world = exchange.rank, exchange.world
         self.rec = ctx.record_bytes
+        self.sync_counters = sync_counters
+        self._pending = []
+        self._epoch = None           # (list epoch, cached receive counts)
 
     def step(self, params5, flags=0, interaction_radius=None, box_cap=1 << 24):
         ctx, ex, r, W, R = self.ctx, self.ex, self.rank, self.world, self.rec
         bb = ex.allreduce_bbox(ctx.local_bbox())
         counts, planes = ctx.slab_plan(bb, W, r, interaction_radius, box_cap)
-        recv_counts = ex.alltoall_counts(counts)          # 3 per rank pair
+        epoch = ctx.slab_list_epoch() if hasattr(ctx, "slab_list_epoch") else -1
+        if epoch >= 0 and self._epoch is not None and self._epoch[0] == epoch:
+            recv_counts = self._epoch[1]                  # refresh sizes are fixed within an epoch
+        else:
+            recv_counts = ex.alltoall_counts(counts)      # 3 per rank pair
+            self._epoch = (epoch, recv_counts) if epoch >= 0 else None
         send_bytes = counts.reshape(W, 3).sum(1) * R
         recv_bytes = recv_counts.reshape(W, 3).sum(1) * R
         send = ex.buffer(int(send_bytes.sum()))
@@ -132,9 +144,28 @@ class SlabRunner:
         recv = ex.alltoall_bytes(send, send_bytes, recv_bytes)
         ctx.slab_unpack(ex.ptr(recv), recv_counts)
         st = ctx.slab_step(params5, flags)
-        tot = ex.allreduce_sum([st.force_evals, st.candidates, st.degenerate_pairs, st.agent_count])
+        local = [st.force_evals, st.candidates, st.degenerate_pairs, st.agent_count]
         rc = recv_counts.reshape(W, 3)
-        return SlabStats(force_evals=int(tot[0]), candidates=int(tot[1]), degenerate_pairs=int(tot[2]),
-                         agents=int(tot[3]), migrated_in=int(rc[:, 0].sum()),
-                         migrated_out=int(counts.reshape(W, 3)[:, 0].sum()), ghosts=int(rc[:, 1:].sum()),
-                         planes=(int(planes[0]), int(planes[1])))
+        stats = SlabStats(force_evals=local[0], candidates=local[1], degenerate_pairs=local[2],
+                          agents=local[3], migrated_in=int(rc[:, 0].sum()),
+                          migrated_out=int(counts.reshape(W, 3)[:, 0].sum()), ghosts=int(rc[:, 1:].sum()),
+                          planes=(int(planes[0]), int(planes[1])))
+        if not self.sync_counters:
+            self._pending.append(stats)
+            return stats
+        tot = ex.allreduce_sum(local)
+        stats.force_evals, stats.candidates, stats.degenerate_pairs, stats.agents = (int(v) for v in tot)
+        return stats
+
+    def collect(self):
+        """Global counters of the steps whose all-reduce was deferred."""
+        if not self._pending:
+            return []
+        loc = np.array([[s.force_evals, s.candidates, s.degenerate_pairs, s.agents] for s in self._pending],
+                       np.int64)
+        tot = np.asarray(self.ex.allreduce_sum(loc.ravel())).reshape(loc.shape)
+        out = self._pending
+        for s, t in zip(out, tot):
+            s.force_evals, s.candidates, s.degenerate_pairs, s.agents = (int(v) for v in t)
+        self._pending = []
+        return out
