@@ -260,8 +260,9 @@ def run_reference(args, rank, world):
 
 def main_slab(args, rank, world, local):
     """N > 1: C5 weak scaling -- each rank starts with its 256-plane x-slab of the
-    (256 G) x 256 x 256 jittered lattice; x-slab decomposition with halo
-    exchange and migration every step (paper_2105_00039_b200/distributed.py)."""
+    (256 G) x 256 x 256 jittered lattice; x-slab decomposition: migration and
+    ghost exchange on rebuild steps, ghost refresh on neighbour-list steps
+    (paper_2105_00039_b200/distributed.py)."""
     import torch
     from paper_2105_00039_b200 import _native
     from paper_2105_00039_b200.distributed import SlabRunner, TorchExchange
@@ -348,7 +349,8 @@ def main_slab(args, rank, world, local):
                                % (world, total, n0),
                    "agents_total": total, "summation": args.summation, "freeze": args.freeze,
                    "l2": "inputs larger than L2 (%.0f MB of agent state per GPU)" % (n0 * 64 / 1e6),
-                   "parallelism": "x-slabs x%d, %s halo exchange + migration every step" % (world, args.exchange)},
+                   "parallelism": "x-slabs x%d over %s: migration + ghost exchange on rebuild steps, ghost refresh on "
+                                  "neighbour-list steps" % (world, args.exchange)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": "sweep7_kernel (per GPU)",
                      "alg_bytes_per_agent": bal, "kernel_ms": t_force, "peak_source": peak_src},

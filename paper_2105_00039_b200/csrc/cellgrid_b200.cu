@@ -5,13 +5,16 @@
 // (reference engine.py:279-341) is:
 //   bbox (from the previous sweep's reduction slots; a standalone pass only
 //   after an upload) -> host geometry (spatial.py:99-116, exact f64) ->
-//   box_keys (+ warp-aggregated counts) -> scan_lookback -> place ->
-//   order_gather (CSR slots by (box, z, uid), fp32 proxies; on a relayout
-//   step the records themselves move into slot order) -> sweep7 (force,
-//   gate, cap, apply, counters, next bbox) -> finish_step (fold the slots).
-// The only host round trip is the 7-double bbox readback: it sizes the grid
-// and raises GridOverflowError before anything is modified, exactly where the
-// reference raises.
+//   box_keys (+ warp-aggregated counts) -> reduce-then-scan -> then either
+//   * a grid sweep: place (CSR slots + fp32 proxies; on a relayout step the
+//     records themselves move into slot order) -> sweep7 (force, gate, cap,
+//     apply, counters, next bbox; optionally also the neighbour lists), or
+//   * a list sweep (list.cuh) while the neighbour lists are valid
+//   -> finish_step (fold the slots).
+// The only host round trip is the 9-double readback (bbox, largest
+// displacement, list overflows): it sizes the grid and raises
+// GridOverflowError before anything is modified, exactly where the reference
+// raises, and decides whether the lists still cover every pair.
 //
 // Storage order.  The reference re-sorts its pool into (Morton code, uid)
 // order on every sort step (engine.py:305-309, morton.py:67-74); only the

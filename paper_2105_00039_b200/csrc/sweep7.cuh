@@ -57,7 +57,7 @@ struct Sweep7Args {
     double shell_lo[3], shell_hi[3];   // bbox shell: old lo + max move, old hi - max move
     int *ovf;                   // slots of agents deferred to the overflow kernel
     unsigned *ovf_count;
-    int n_owned;                // storage indices >= n_owned are ghosts (slab halo): not targets
+    int n_owned;                // targets: [own_lo, own_lo + n_owned); the rest are slab ghosts (candidates)
     bool uid32;                 // every uid < 2^32: survivor sort keys come from the proxies
     int own_lo;                 // targets are storage indices [own_lo, own_lo + n_owned): a relaid
                                 // slab sub-grid keeps its lo ghosts in front of the owned agents
