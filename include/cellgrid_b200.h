@@ -98,6 +98,12 @@ int cg_upload(cg_context *ctx, int64_t n, const void *px, const void *py, const 
 int cg_download(cg_context *ctx, void *px, void *py, void *pz, void *diameter,
                 void *adherence, uint64_t *uid, void *dx, void *dy, void *dz);
 int64_t cg_count(const cg_context *ctx);
+/* cg_step followed by cg_download, with the transfers overlapped: the columns
+ * the step does not change (diameter, adherence, uid, in the reference's new
+ * order) are copied to the host while the sweep runs.  Same results. */
+int cg_step_download(cg_context *ctx, const double params[5], double interaction_radius, int64_t box_cap,
+                     int flags, cg_step_stats *stats, void *px, void *py, void *pz, void *diameter,
+                     void *adherence, uint64_t *uid, void *dx, void *dy, void *dz);
 /* Kernels launched by this context so far (evidence for bench gpu_launches). */
 int64_t cg_launch_count(const cg_context *ctx);
 /* Page-locked host memory for staging pool columns (NULL on failure). */

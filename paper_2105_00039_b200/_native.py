@@ -31,7 +31,7 @@ EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_
             "cg_host_alloc", "cg_host_free", "cg_record_bytes", "cg_reserve", "cg_local_bbox",
             "cg_slab_plan", "cg_slab_pack", "cg_slab_unpack",
             "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill",
-            "cg_list_stats", "cg_slab_list_epoch")
+            "cg_list_stats", "cg_slab_list_epoch", "cg_step_download")
 
 
 class GridOverflowError(RuntimeError):
@@ -100,6 +100,8 @@ def load():
         "cg_force_phase": ([_P, _I64] + [_P] * 7 + [_I64] * 3 + [_P] * 5, ctypes.c_int),
         "cg_neighbor_counts": ([_P, ctypes.c_double, _P], ctypes.c_int),
         "cg_list_stats": ([_P, _P], ctypes.c_int),
+        "cg_step_download": ([_P, _P, ctypes.c_double, _I64, ctypes.c_int, ctypes.POINTER(StepStatsC)]
+                             + [_P] * 9, ctypes.c_int),
         "cg_slab_list_epoch": ([_P], _I64),
         "cg_neighbor_fill": ([_P, ctypes.c_double, _P, _P], ctypes.c_int),
         "cg_record_bytes": ([_P], _I64),
@@ -200,6 +202,24 @@ class Context:
                 args.append(None)
         check(load().cg_download(self.h, *args), self.h)
         return out
+
+    def step_download(self, params5, interaction_radius=None, box_cap=1 << 24, flags=0, into=None):
+        """step + download with the unchanged columns copied during the sweep
+        (cg_step_download); returns (stats, columns)."""
+        p = np.ascontiguousarray(params5, np.float64)
+        ir = float("nan") if interaction_radius is None else float(interaction_radius)
+        out, args = {}, []
+        for name in ("px", "py", "pz", "diameter", "adherence", "uid", "dx", "dy", "dz"):
+            dst = None if into is None else into.get(name)
+            if dst is None or dst.shape[0] != self.n:
+                dst = np.empty(self.n, np.uint64 if name == "uid" else self.dtype)
+            out[name] = dst
+            args.append(ptr(dst))
+        st = StepStatsC()
+        check(load().cg_step_download(self.h, ptr(p), ir, int(box_cap), int(flags), ctypes.byref(st), *args),
+              self.h)
+        self.steps += 1
+        return st, out
 
     def step(self, params5, interaction_radius=None, box_cap=1 << 24, flags=0, wait=True):
         p = np.ascontiguousarray(params5, np.float64)

@@ -106,6 +106,14 @@ struct cg_context {
     cg_step_stats ring[kRing];
     cudaEvent_t ev[kRing][5];
     cudaStream_t copy_stream = nullptr;       // download: D2H overlapped with the unpack kernels
+    // cg_step_download: diameter / adherence / uid leave during the sweep
+    struct Early {
+        bool want = false, done = false;
+        void *dst[3] = {nullptr, nullptr, nullptr};   // diameter, adherence, uid (host)
+        char *buf = nullptr;
+        size_t bytes = 0;
+        cudaEvent_t grid_done = nullptr, ready = nullptr;
+    } early;
     cudaEvent_t dl_ready[9] = {}, dl_done[9] = {}, dl_start = nullptr;
     int64_t steps_done = 0;
     int64_t launches = 0;
@@ -383,11 +391,11 @@ static int standalone_bbox(cg_context *c)
 
 // The reference's storage order (see header comment): sort storage indices
 // by uid, then stably by the Morton rank of their box at the last sort step.
-static int materialize_presentation(cg_context *c)
+static int materialize_presentation(cg_context *c, cudaStream_t st = nullptr)
 {
     if (c->pres_state != PRES_PENDING) return CG_OK;
     const Geometry &g = c->geo_sort;
-    cudaStream_t st = c->stream;
+    if (!st) st = c->stream;
     const int n = (int)c->n;
     if (c->table_dims[0] != g.dimx || c->table_dims[1] != g.dimy || c->table_dims[2] != g.dimz) {
         int rc = ensure_boxes(c, g.nb);
@@ -811,6 +819,74 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     return CG_OK;
 }
 
+static int ensure_copy_stream(cg_context *c)
+{
+    if (c->copy_stream) return CG_OK;
+    // highest priority: the reorder kernels of an early download go ahead of
+    // the sweep's blocks, so the PCIe transfer starts while the sweep runs
+    int lo = 0, hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->copy_stream, cudaStreamNonBlocking, hi));
+    for (int k = 0; k < 9; ++k) {
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_ready[k], cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_done[k], cudaEventDisableTiming));
+    }
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_start, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->early.grid_done, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->early.ready, cudaEventDisableTiming));
+    return CG_OK;
+}
+
+// cg_step_download, once the grid of the step is built: the reference order
+// (pres) is materialised and the columns the sweep does not change --
+// diameter, adherence, uid -- are reordered and copied to the host on the
+// copy stream while the sweep runs on the context stream.
+template <typename T>
+static int early_download(cg_context *c)
+{
+    int rc;
+    if ((rc = ensure_copy_stream(c))) return rc;
+    const int64_t n = c->n;
+    const size_t need = 2 * 8 * (size_t)n;
+    if (need > c->early.bytes) {
+        if (c->early.buf) cudaFree(c->early.buf);
+        c->early.buf = nullptr;
+        CUDA_TRY(c, cudaMalloc(&c->early.buf, need));
+        c->early.bytes = need;
+    }
+    cudaStream_t st = c->stream, cs = c->copy_stream;
+    CUDA_TRY(c, cudaEventRecord(c->early.grid_done, st));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->early.grid_done, 0));
+    if ((rc = materialize_presentation(c, cs))) return rc;
+    const int *pres = c->pres_state == PRES_IDENTITY ? nullptr : c->b.pres;
+    char *buf[3] = {c->early.buf, c->early.buf + 8 * (size_t)n, (char *)c->b.stage};
+    const int nb = cdiv(n, kThreads);
+    if (c->early.dst[0])
+        unpack_component<T><<<nb, kThreads, 0, cs>>>((int)n, (const Rec<T> *)c->b.rec[c->cur_pos], 3, pres,
+                                                     (T *)buf[0]);
+    const void *src[3] = {nullptr, c->b.adh[c->cur_attr], c->b.uid[c->cur_attr]};
+    for (int k = 1; k < 3; ++k) {
+        if (!c->early.dst[k]) continue;
+        if (!pres) {
+            buf[k] = (char *)src[k];
+        } else if (k == 2 || sizeof(T) == 8) {
+            scatter_by<unsigned long long><<<nb, kThreads, 0, cs>>>((int)n, pres, (const unsigned long long *)src[k],
+                                                                    (unsigned long long *)buf[k]);
+        } else {
+            scatter_by<unsigned><<<nb, kThreads, 0, cs>>>((int)n, pres, (const unsigned *)src[k], (unsigned *)buf[k]);
+        }
+    }
+    LAUNCH_CHECK(c);
+    c->launches += 3;
+    for (int k = 0; k < 3; ++k)
+        if (c->early.dst[k])
+            CUDA_TRY(c, cudaMemcpyAsync(c->early.dst[k], buf[k], (k == 2 ? 8 : sizeof(T)) * (size_t)n,
+                                        cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(c, cudaEventRecord(c->early.ready, cs));
+    c->early.done = true;
+    return CG_OK;
+}
+
 template <typename T>
 static int step_impl(cg_context *c, const double params[5], double ir, int64_t box_cap, int flags,
                      int64_t *step_id)
@@ -890,6 +966,7 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
         } else if (relayout) {
             c->pres_state = PRES_PENDING;
         }
+        if (c->early.want && (rc = early_download<T>(c))) return rc;
         build = build && !c->last_dense;
         c->list_valid = false;
         if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
@@ -1539,6 +1616,9 @@ void cg_destroy(cg_context *c)
             if (c->ev[r][e]) cudaEventDestroy(c->ev[r][e]);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->early.buf) cudaFree(c->early.buf);
+    if (c->early.grid_done) cudaEventDestroy(c->early.grid_done);
+    if (c->early.ready) cudaEventDestroy(c->early.ready);
     for (int k = 0; k < 9; ++k) {
         if (c->dl_ready[k]) cudaEventDestroy(c->dl_ready[k]);
         if (c->dl_done[k]) cudaEventDestroy(c->dl_done[k]);
@@ -1665,24 +1745,15 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
     return CG_OK;
 }
 
-int cg_download(cg_context *c, void *px, void *py, void *pz, void *diameter, void *adherence,
-                uint64_t *uid, void *dx, void *dy, void *dz)
+static int download_cols(cg_context *c, void *const dst_in[9])
 {
-    if (!c) return CG_ERR_VALUE;
-    CUDA_TRY(c, cudaSetDevice(c->device));
     const int64_t n = c->n_owned;   // a slab keeps its ghosts after the owned agents
     if (n == 0) return CG_OK;
     int rc = materialize_presentation(c);
     if (rc) return rc;
-    if (!c->copy_stream) {
-        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-        for (int k = 0; k < 9; ++k) {
-            CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_ready[k], cudaEventDisableTiming));
-            CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_done[k], cudaEventDisableTiming));
-        }
-        CUDA_TRY(c, cudaEventCreateWithFlags(&c->dl_start, cudaEventDisableTiming));
-    }
-    void *dst[9] = {px, py, pz, diameter, adherence, uid, dx, dy, dz};
+    if ((rc = ensure_copy_stream(c))) return rc;
+    void *dst[9];
+    for (int k = 0; k < 9; ++k) dst[k] = dst_in[k];
     const void *src[9] = {nullptr, nullptr, nullptr, nullptr, c->b.adh[c->cur_attr], c->b.uid[c->cur_attr],
                           c->b.disp[0], c->b.disp[1], c->b.disp[2]};
     cudaStream_t st = c->stream, cs = c->copy_stream;
@@ -1735,6 +1806,37 @@ int cg_download(cg_context *c, void *px, void *py, void *pz, void *diameter, voi
     CUDA_TRY(c, cudaStreamSynchronize(cs));
     CUDA_TRY(c, cudaStreamSynchronize(st));
     return CG_OK;
+}
+
+int cg_download(cg_context *c, void *px, void *py, void *pz, void *diameter, void *adherence,
+                uint64_t *uid, void *dx, void *dy, void *dz)
+{
+    if (!c) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    void *dst[9] = {px, py, pz, diameter, adherence, uid, dx, dy, dz};
+    return download_cols(c, dst);
+}
+
+int cg_step_download(cg_context *c, const double params[5], double interaction_radius, int64_t box_cap, int flags,
+                     cg_step_stats *stats, void *px, void *py, void *pz, void *diameter, void *adherence,
+                     uint64_t *uid, void *dx, void *dy, void *dz)
+{
+    if (!c) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    c->early = cg_context::Early{false, false, {diameter, adherence, uid}, c->early.buf, c->early.bytes,
+                                 c->early.grid_done, c->early.ready};
+    c->early.want = c->n == c->n_owned && c->n > 0;
+    int rc = cg_step(c, params, interaction_radius, box_cap, flags, stats);
+    const bool early = c->early.done;
+    c->early.want = c->early.done = false;
+    if (rc) {
+        if (early) cudaStreamSynchronize(c->copy_stream);
+        return rc;
+    }
+    void *dst[9] = {px, py, pz, early ? nullptr : diameter, early ? nullptr : adherence, early ? nullptr : (void *)uid,
+                    dx, dy, dz};
+    if (early) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->early.ready, 0));   // pres + early buffers
+    return download_cols(c, dst);
 }
 
 int cg_step(cg_context *c, const double params[5], double interaction_radius, int64_t box_cap,

@@ -274,10 +274,10 @@ _POOL_COLS = (("px", "position_x"), ("py", "position_y"), ("pz", "position_z"),
               ("dx", "displacement_x"), ("dy", "displacement_y"), ("dz", "displacement_z"))
 
 
-def _download(ctx, pool):
-    """Write the device pool back into the host pool's own arrays where they are
-    reusable (contiguous, writeable, right dtype/length) -- so pinned host
-    columns stay pinned -- else into fresh arrays."""
+def _reusable(ctx, pool):
+    """The host pool's own arrays where a download can write in place
+    (contiguous, writeable, right dtype/length) -- so pinned host columns
+    stay pinned."""
     into = {}
     for key, attr in _POOL_COLS:
         a = getattr(pool, attr, None)
@@ -285,10 +285,18 @@ def _download(ctx, pool):
         if (isinstance(a, np.ndarray) and a.dtype == want and a.shape == (ctx.n,)
                 and a.flags.c_contiguous and a.flags.writeable):
             into[key] = a
-    cols = ctx.download(into=into)
+    return into
+
+
+def _assign(pool, cols):
     pool.position_x, pool.position_y, pool.position_z = cols["px"], cols["py"], cols["pz"]
     pool.diameter, pool.adherence, pool.uid = cols["diameter"], cols["adherence"], cols["uid"]
     pool.displacement_x, pool.displacement_y, pool.displacement_z = cols["dx"], cols["dy"], cols["dz"]
+
+
+def _download(ctx, pool):
+    """Write the device pool back into the host pool (in place where possible)."""
+    _assign(pool, ctx.download(into=_reusable(ctx, pool)))
 
 
 def _empty_stats(step_index):
@@ -326,9 +334,10 @@ def step(pool, config: SimulationConfig, step_index=0):
         return st
     ctx = _context(config.strategy, pool.dtype)
     _upload(ctx, pool)
-    st = ctx.step(params_vector(config.force_params), config.interaction_radius,
-                  DEFAULT_BOX_CAP, step_flags(config, step_index))
-    _download(ctx, pool)
+    # the step and the download of its result, transfers overlapped with the sweep
+    st, cols = ctx.step_download(params_vector(config.force_params), config.interaction_radius,
+                                 DEFAULT_BOX_CAP, step_flags(config, step_index), into=_reusable(ctx, pool))
+    _assign(pool, cols)
     out = _to_stats(st, step_index, pool.precision.itemsize)
     out.divisions = divisions
     out.t_behavior = t_behavior

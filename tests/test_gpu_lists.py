@@ -125,3 +125,29 @@ def test_list_overflow_falls_back(cuda_required):
         assert a[0] == b[0]
         for col in a[1]:
             assert np.array_equal(a[1][col], b[1][col])
+
+
+@pytest.mark.parametrize("sort_every", [1, 0])
+@pytest.mark.parametrize("name,pool", POOLS, ids=[p[0] for p in POOLS])
+def test_step_download_equals_step_then_download(cuda_required, name, pool, sort_every):
+    """cg_step_download (transfers overlapped with the sweep) returns exactly
+    what cg_step followed by cg_download returns, step after step (uploads
+    between steps, as engine.step does)."""
+    from paper_2105_00039_b200 import _native as N
+    a, b = N.Context(0, pool.dtype), N.Context(0, pool.dtype)
+    try:
+        cur_a = cur_b = {"px": pool.position_x, "py": pool.position_y, "pz": pool.position_z,
+                         "diameter": pool.diameter, "adherence": pool.adherence, "uid": pool.uid}
+        for k in range(3):
+            flags = N.CG_STEP_SORT if sort_every and k % sort_every == 0 else 0
+            a.upload(cur_a["px"], cur_a["py"], cur_a["pz"], cur_a["diameter"], cur_a["adherence"], cur_a["uid"])
+            b.upload(cur_b["px"], cur_b["py"], cur_b["pz"], cur_b["diameter"], cur_b["adherence"], cur_b["uid"])
+            sa, cur_a = a.step_download(PARAMS5, None, 1 << 24, flags)
+            sb = b.step(PARAMS5, None, 1 << 24, flags)
+            cur_b = b.download()
+            assert (sa.force_evals, sa.candidates) == (sb.force_evals, sb.candidates)
+            for col in cur_b:
+                assert np.array_equal(cur_a[col], cur_b[col]), (name, k, col)
+    finally:
+        a.close()
+        b.close()

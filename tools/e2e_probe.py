@@ -40,6 +40,19 @@ for r in range(reps + 1):
 for k, v in t.items():
     print("%-9s %8.2f ms" % (k, 1e3 * np.median(v)))
 print("total     %8.2f ms" % (1e3 * sum(np.median(v) for v in t.values())))
+# the fused call: step + download with the unchanged columns copied during the sweep
+tf = []
+for r in range(reps + 1):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.upload(cols["px"], cols["py"], cols["pz"], cols["diameter"], cols["adherence"], cols["uid"])
+    t1 = time.perf_counter()
+    ctx.step_download(P, None, 1 << 24, _native.CG_STEP_SORT, into=outs)
+    t2 = time.perf_counter()
+    if r:
+        tf.append(t2 - t1)
+print("step_download %8.2f ms (step + download %.2f ms)" % (1e3 * np.median(tf),
+                                                          1e3 * (np.median(t["step"]) + np.median(t["download"]))))
 # raw pinned copy rates
 n = pool.count
 h = torch.empty(n * 6, dtype=torch.float64, pin_memory=True)
