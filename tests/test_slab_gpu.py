@@ -61,7 +61,8 @@ def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1):
 
 @pytest.mark.parametrize("world,summation,skin,params", [
     (2, 0, 0, (2.0, 1.0, 0.01, 3.0, 1.0)), (3, 1, 0, (2.0, 1.0, 0.01, 3.0, 1.0)),
-    (2, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)), (3, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0))])
+    (2, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)), (3, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)),
+    (5, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0))])   # 5 slabs of ~4 planes: ghost bands reach two ranks away
 def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, params):
     """skin 0: a full exchange every step; skin -1: neighbour lists, the
     partition frozen and the ghosts refreshed between rebuilds (small
