@@ -151,3 +151,33 @@ def test_step_download_equals_step_then_download(cuda_required, name, pool, sort
     finally:
         a.close()
         b.close()
+
+
+def test_lists_long_run_matches_oracle(cuda_required):
+    """60 chained uid-order steps of a 32,768-agent jittered lattice (several
+    list epochs and rebuilds): lists on, lists off and the C oracle agree bit
+    for bit at the end (positions, displacements, storage order)."""
+    from paper_2105_00039_b200 import _native as N
+    from paper_2105_00039_b200.mechanics import ForceParams
+    from paper_2105_00039_b200.pool import AgentPool
+    from paper_2105_00039_b200.workloads import jittered_lattice_positions
+    pool = AgentPool.from_arrays(jittered_lattice_positions(32, 8.0, 1.0, 11), 10.0, 0.4)
+    params = ForceParams(timestep=0.02)
+    p5 = np.array([params.kappa, params.gamma, params.timestep, params.max_displacement, params.adherence_scale])
+    outs = []
+    for skin in (-1, 0):
+        ctx = N.Context(0, pool.dtype)
+        ctx.set_option(N.CG_OPT_SUMMATION, 0)
+        ctx.set_option(N.CG_OPT_LIST_SKIN, skin)
+        ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+        evals = [ctx.step(p5, None, 1 << 24, N.CG_STEP_SORT).force_evals for _ in range(60)]
+        outs.append((evals, ctx.download(), ctx.list_stats()))
+        ctx.close()
+    assert outs[0][2]["builds"] >= 3 and outs[0][2]["list_steps"] >= 30, outs[0][2]
+    ref = pool.copy()
+    ref_evals = [oracle.step(ref, params, sort=True, threads=8).force_evals for _ in range(60)]
+    assert outs[0][0] == outs[1][0] == ref_evals
+    for cols, _ in ((outs[0][1], 0), (outs[1][1], 1)):
+        assert np.array_equal(cols["uid"], ref.uid)
+        for a, b in (("px", "position_x"), ("py", "position_y"), ("pz", "position_z"), ("dx", "displacement_x")):
+            assert np.array_equal(cols[a], getattr(ref, b)), a
