@@ -773,11 +773,17 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     unsigned long long *stat = c->stat_dev + slot * kStatSlots;
     CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
     const int cp = c->cur_pos, ca = c->cur_attr;
-    box_keys<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, g, 1.0 / g.L, (const Rec<T> *)c->b.rec[cp], c->count,
-                                                        c->b.key_rank);
-    LAUNCH_CHECK(c);
-    c->launches += 1;
-    if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
+    // a recorded step (per-agent m / nk, grid export) builds the CSR first;
+    // otherwise the box counting runs inside the list sweep (FUSED) and the
+    // candidates counter and grid statistics come from one pass over the boxes
+    const bool fused = !record;
+    if (!fused) {
+        box_keys<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(n, g, 1.0 / g.L, (const Rec<T> *)c->b.rec[cp], c->count,
+                                                            c->b.key_rank);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
+    }
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
     ListArgs<T> A{};
@@ -800,18 +806,29 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     A.rec_m = record ? c->b.rec_m : nullptr;
     A.rec_nk = record ? c->b.rec_nk : nullptr;
     A.pkey = sort ? c->b.pkey[ca] : nullptr;
+    A.count = c->count;
+    A.invL = 1.0 / g.L;
     A.slots = c->slots;
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
-    list_sweep_kernel<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);
+    if (fused) {
+        list_sweep_kernel<T, true><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);
+        box_stencil_pass<<<std::min(cdiv(g.nb, kThreads), 148 * 8), kThreads, 0, st>>>(g, c->bd, c->count, c->slots,
+                                                                                         stat);
+        CUDA_TRY(c, cudaMemsetAsync(c->count, 0, sizeof(int) * (size_t)g.nb, st));   // zero for the next step
+        c->launches += 2;
+    } else {
+        list_sweep_kernel<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);
+        c->launches += 1;
+    }
     finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, stat, c->bbox_dev,
                                          FINISH_COUNTERS | (freeze ? 0 : FINISH_BBOX));
     LAUNCH_CHECK(c);
-    c->launches += 2;
+    c->launches += 1;
     if (!freeze)
         CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
     c->bbox_valid = true;
-    c->have_grid = true;
-    c->relaid = false;      // slot arrays are not rebuilt: exports use key_rank
+    c->have_grid = !fused;   // a fused step keeps no slot-level CSR to export
+    c->relaid = false;       // slot arrays are not rebuilt: exports use key_rank
     c->last_dense = false;
     if (sort) c->geo_sort = g;
     c->list_life++;

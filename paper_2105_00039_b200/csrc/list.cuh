@@ -40,6 +40,8 @@ struct ListArgs {
     Rec<T> *new_rec;          // nullptr when frozen
     int *rec_m, *rec_nk;      // nullptr unless recording
     int *pkey;                // this step's box (sort steps), nullptr otherwise
+    int *count;               // FUSED: per-box counts accumulated here (zero on entry)
+    double invL;              // FUSED: 1 / box length
     unsigned long long *slots;
     double shell_lo[3], shell_hi[3];
 };
@@ -64,20 +66,40 @@ __device__ __noinline__ void degenerate_pair(uint64_t ui, uint64_t uj, T mag, T 
 #define CG_LIST_MINB 4
 #endif
 
-template <typename T>
+// FUSED: the step's box counting is done here (box id of the current
+// position, one atomic per run of equal keys in the warp) instead of in a
+// separate box_keys pass; m and the grid statistics then come from the
+// per-box pass box_stencil_pass (a step without CG_STEP_RECORD).
+template <typename T, bool FUSED = false>
 __global__ void __launch_bounds__(kThreads, CG_LIST_MINB) list_sweep_kernel(ListArgs<T> A)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int a = A.own_lo + t;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
     float dmax2 = 0.f;
+    if (FUSED) {
+        const int lane = threadIdx.x & 31;
+        int flat = -1 - lane;   // distinct dummy keys past n
+        if (t < A.n) {
+            const Rec<T> r = A.rec[a];
+            flat = flat_box_fast(A.g, A.invL, r.x, r.y, r.z);
+            if (A.pkey) A.pkey[a] = flat;
+        }
+        const int prev = __shfl_up_sync(0xffffffffu, flat, 1);
+        const bool start = lane == 0 || prev != flat;
+        const unsigned starts = __ballot_sync(0xffffffffu, start);
+        const unsigned after = starts & ~(0xffffffffu >> (31 - lane));   // run starts above this lane
+        const int run_end = after ? __ffs(after) - 1 : 32;
+        if (start && t < A.n) atomicAdd(A.count + flat, run_end - lane);
+    }
     if (t < A.n) {
+        int m = -1;
+        if (!FUSED) {
         const int key = A.key_rank[a].x;
         if (A.pkey) A.pkey[a] = key;
         int ix, iy, iz;
         decode_box(A.bd, key, ix, iy, iz);
         // m: agents of the 27 clamped boxes minus self (_gather_stencil)
-        int m = -1;
         {
             const int z0 = max(iz - 1, 0), z1 = min(iz + 1, A.g.dimz - 1);
 #pragma unroll
@@ -92,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, CG_LIST_MINB) list_sweep_kernel(List
                     m += __ldg(A.off + base + z1 + 1) - __ldg(A.off + base + z0);
                 }
             }
+        }
         }
         const T half = T(0.5), zero = A.p.zero;
         const Rec<T> me = A.rec[a];
@@ -189,16 +212,52 @@ __global__ void __launch_bounds__(kThreads, CG_LIST_MINB) list_sweep_kernel(List
                 if (p3[q] >= A.shell_hi[q]) atomicMax(slot + 3 + q, enc_ordered(p3[q]));
             }
         }
-        if (A.rec_m) {
+        if (!FUSED && A.rec_m) {
             A.rec_m[a] = m;
             A.rec_nk[a] = nk;
         }
-        c_m = (unsigned)m;
+        c_m = FUSED ? 0u : (unsigned)m;
         c_nk = (unsigned)nk;
         c_nd = (unsigned)nd;
     }
     warp_counters(A.slots, c_m, c_nk, c_nd);
     warp_dmax(A.slots, dmax2);
+}
+
+// After a FUSED list sweep: per occupied box b, S_b = agents of its clamped
+// 27-box stencil; candidates += count_b * (S_b - 1) (every agent of b has
+// m = S_b - 1, _gather_stencil), occupied boxes and the largest occupancy
+// (stat[0], stat[1]).  Grid-stride, block-reduced.
+__global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDecode bd, const int *__restrict__ count,
+                                                             unsigned long long *__restrict__ slots,
+                                                             unsigned long long *__restrict__ stat)
+{
+    unsigned long long cand = 0, occ = 0, mx = 0;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < g.nb; b += gridDim.x * blockDim.x) {
+        const int c = __ldg(count + b);
+        if (!c) continue;
+        int ix, iy, iz;
+        decode_box(bd, b, ix, iy, iz);
+        const int z0 = max(iz - 1, 0), z1 = min(iz + 1, g.dimz - 1);
+        int S = 0;
+        for (int nx = max(ix - 1, 0); nx <= min(ix + 1, g.dimx - 1); ++nx)
+            for (int ny = max(iy - 1, 0); ny <= min(iy + 1, g.dimy - 1); ++ny) {
+                const int base = (nx * g.dimy + ny) * g.dimz;
+                for (int nz = z0; nz <= z1; ++nz) S += __ldg(count + base + nz);
+            }
+        cand += (unsigned long long)c * (unsigned long long)(S - 1);
+        ++occ;
+        mx = max(mx, (unsigned long long)c);
+    }
+    cand = warp_sum(cand);
+    occ = warp_sum(occ);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) {
+        if (cand) atomicAdd(slots + (blockIdx.x % kSlots) * kSlotWords + 7, cand);
+        if (occ) atomicAdd(stat + 0, occ);
+        if (mx) atomicMax(stat + 1, mx);
+    }
 }
 
 }  // namespace cg

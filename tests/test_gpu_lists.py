@@ -170,12 +170,18 @@ def test_lists_long_run_matches_oracle(cuda_required):
         ctx.set_option(N.CG_OPT_SUMMATION, 0)
         ctx.set_option(N.CG_OPT_LIST_SKIN, skin)
         ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
-        evals = [ctx.step(p5, None, 1 << 24, N.CG_STEP_SORT).force_evals for _ in range(60)]
+        sts = [ctx.step(p5, None, 1 << 24, N.CG_STEP_SORT) for _ in range(60)]
+        evals = [(s.force_evals, s.candidates, s.degenerate_pairs, s.grid_occupied_boxes, s.grid_max_occupancy)
+                 for s in sts]
         outs.append((evals, ctx.download(), ctx.list_stats()))
         ctx.close()
     assert outs[0][2]["builds"] >= 3 and outs[0][2]["list_steps"] >= 30, outs[0][2]
     ref = pool.copy()
-    ref_evals = [oracle.step(ref, params, sort=True, threads=8).force_evals for _ in range(60)]
+    ref_evals = []
+    for _ in range(60):
+        r = oracle.step(ref, params, sort=True, threads=8)
+        ref_evals.append((r.force_evals, r.candidates, r.degenerate_pairs, int(np.count_nonzero(r.box_count)),
+                          int(r.box_count.max())))
     assert outs[0][0] == outs[1][0] == ref_evals
     for cols, _ in ((outs[0][1], 0), (outs[1][1], 1)):
         assert np.array_equal(cols["uid"], ref.uid)
