@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--relayout-every", type=int, default=1,
                     help="move records into slot order on every k-th sort step")
     ap.add_argument("--sort-every", type=int, default=1)
+    ap.add_argument("--list-skin", type=int, default=-1,
+                    help="CG_OPT_LIST_SKIN: -1 auto (0.07 box lengths), 0 off, k > 0 = k/1000 length units")
     ap.add_argument("--freeze", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -388,6 +390,7 @@ def main():
     ctx = _native.Context(local, pool.dtype)
     ctx.set_option(_native.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[args.summation])
     ctx.set_option(_native.CG_OPT_RELAYOUT_EVERY, args.relayout_every)
+    ctx.set_option(_native.CG_OPT_LIST_SKIN, args.list_skin)
     ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence,
                pool.uid)
     params = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
