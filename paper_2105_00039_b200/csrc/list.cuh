@@ -227,24 +227,40 @@ __global__ void __launch_bounds__(kThreads, CG_LIST_MINB) list_sweep_kernel(List
 // After a FUSED list sweep: per occupied box b, S_b = agents of its clamped
 // 27-box stencil; candidates += count_b * (S_b - 1) (every agent of b has
 // m = S_b - 1, _gather_stencil), occupied boxes and the largest occupancy
-// (stat[0], stat[1]).  Grid-stride, block-reduced.
+// (stat[0], stat[1]).  Separable: box_sum_yz writes the 3 x 3 (y, z) window
+// sums, box_stencil_pass adds the three x planes (coalesced, z fastest).
+__global__ void __launch_bounds__(kThreads) box_sum_yz(Geometry g, BoxDecode bd, const int *__restrict__ count,
+                                                       int *__restrict__ syz)
+{
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < g.nb; b += gridDim.x * blockDim.x) {
+        int ix, iy, iz;
+        decode_box(bd, b, ix, iy, iz);
+        int v = 0;
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+            if ((unsigned)(iy + dy) >= (unsigned)g.dimy) continue;
+#pragma unroll
+            for (int dz = -1; dz <= 1; ++dz)
+                if ((unsigned)(iz + dz) < (unsigned)g.dimz) v += __ldg(count + b + dy * g.dimz + dz);
+        }
+        syz[b] = v;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDecode bd, const int *__restrict__ count,
+                                                             const int *__restrict__ syz,
                                                              unsigned long long *__restrict__ slots,
                                                              unsigned long long *__restrict__ stat)
 {
     unsigned long long cand = 0, occ = 0, mx = 0;
+    const int plane = g.dimy * g.dimz;
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < g.nb; b += gridDim.x * blockDim.x) {
         const int c = __ldg(count + b);
         if (!c) continue;
-        int ix, iy, iz;
-        decode_box(bd, b, ix, iy, iz);
-        const int z0 = max(iz - 1, 0), z1 = min(iz + 1, g.dimz - 1);
-        int S = 0;
-        for (int nx = max(ix - 1, 0); nx <= min(ix + 1, g.dimx - 1); ++nx)
-            for (int ny = max(iy - 1, 0); ny <= min(iy + 1, g.dimy - 1); ++ny) {
-                const int base = (nx * g.dimy + ny) * g.dimz;
-                for (int nz = z0; nz <= z1; ++nz) S += __ldg(count + base + nz);
-            }
+        const int ix = b / plane;
+        int S = __ldg(syz + b);
+        if (ix > 0) S += __ldg(syz + b - plane);
+        if (ix + 1 < g.dimx) S += __ldg(syz + b + plane);
         cand += (unsigned long long)c * (unsigned long long)(S - 1);
         ++occ;
         mx = max(mx, (unsigned long long)c);
