@@ -815,7 +815,6 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
         const int gb = std::min(cdiv(g.nb, kThreads), 148 * 8);
         box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);   // offsets are unused on a fused step
         box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset, c->slots, stat);
-        CUDA_TRY(c, cudaMemsetAsync(c->count, 0, sizeof(int) * (size_t)g.nb, st));   // zero for the next step
         c->launches += 3;
     } else {
         list_sweep_kernel<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);

@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(kThreads, CG_LIST_MINB) list_sweep_kernel(List
 // 27-box stencil; candidates += count_b * (S_b - 1) (every agent of b has
 // m = S_b - 1, _gather_stencil), occupied boxes and the largest occupancy
 // (stat[0], stat[1]).  Separable: box_sum_yz writes the 3 x 3 (y, z) window
-// sums, box_stencil_pass adds the three x planes (coalesced, z fastest).
+// sums, box_stencil_pass adds the three x planes (coalesced, z fastest) and
+// resets the counts to zero for the next step.
 __global__ void __launch_bounds__(kThreads) box_sum_yz(Geometry g, BoxDecode bd, const int *__restrict__ count,
                                                        int *__restrict__ syz)
 {
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) box_sum_yz(Geometry g, BoxDecode bd,
     }
 }
 
-__global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDecode bd, const int *__restrict__ count,
+__global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDecode bd, int *__restrict__ count,
                                                              const int *__restrict__ syz,
                                                              unsigned long long *__restrict__ slots,
                                                              unsigned long long *__restrict__ stat)
@@ -255,8 +256,9 @@ __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDeco
     unsigned long long cand = 0, occ = 0, mx = 0;
     const int plane = g.dimy * g.dimz;
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < g.nb; b += gridDim.x * blockDim.x) {
-        const int c = __ldg(count + b);
+        const int c = count[b];
         if (!c) continue;
+        count[b] = 0;   // the counts start the next step at zero
         const int ix = b / plane;
         int S = __ldg(syz + b);
         if (ix > 0) S += __ldg(syz + b - plane);
