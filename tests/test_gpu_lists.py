@@ -32,7 +32,7 @@ def _pools():
 POOLS = list(_pools())
 
 
-def _run(pool, skin, steps, summation, sort_every=1, freeze_at=()):
+def _run(pool, skin, steps, summation, sort_every=1, freeze_at=(), record=True):
     from paper_2105_00039_b200 import _native as N
     ctx = N.Context(0, pool.dtype)
     ctx.set_option(N.CG_OPT_SUMMATION, summation)
@@ -40,16 +40,19 @@ def _run(pool, skin, steps, summation, sort_every=1, freeze_at=()):
     ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
     out = []
     for k in range(steps):
-        flags = N.CG_STEP_RECORD
+        flags = N.CG_STEP_RECORD if record else 0
         if sort_every and k % sort_every == 0:
             flags |= N.CG_STEP_SORT
         if k in freeze_at:
             flags |= N.CG_STEP_FREEZE
         st = ctx.step(PARAMS5, None, 1 << 24, flags)
         cols = ctx.download()
-        m, nk = ctx.record_export()
-        nb = int(np.prod(list(st.grid_dims)))
-        bi, bc = ctx.grid_export(nb)
+        if record:
+            m, nk = ctx.record_export()
+            nb = int(np.prod(list(st.grid_dims)))
+            bi, bc = ctx.grid_export(nb)
+        else:
+            m = nk = bi = bc = np.zeros(0)
         out.append(((st.force_evals, st.candidates, st.degenerate_pairs, st.grid_occupied_boxes,
                      st.grid_max_occupancy, tuple(st.grid_dims)), cols, m, nk, bi, bc))
     stats = ctx.list_stats()
@@ -187,3 +190,18 @@ def test_lists_long_run_matches_oracle(cuda_required):
         assert np.array_equal(cols["uid"], ref.uid)
         for a, b in (("px", "position_x"), ("py", "position_y"), ("pz", "position_z"), ("dx", "displacement_x")):
             assert np.array_equal(cols[a], getattr(ref, b)), a
+
+
+@pytest.mark.parametrize("name,pool", POOLS, ids=[p[0] for p in POOLS])
+def test_fused_list_steps_change_nothing(cuda_required, name, pool):
+    """Steps without CG_STEP_RECORD take the fused list path (box counting in
+    the list sweep, candidates and statistics from the box-stencil pass):
+    counters, grid statistics and every column equal the list-free run."""
+    got, st = _run(pool, -1, 12, 0, freeze_at=(5,), record=False)
+    ref, _ = _run(pool, 0, 12, 0, freeze_at=(5,), record=False)
+    if name.startswith("lattice"):
+        assert st["list_steps"] > 0, st
+    for k, (a, b) in enumerate(zip(got, ref)):
+        assert a[0] == b[0], (name, k)
+        for col in a[1]:
+            assert np.array_equal(a[1][col], b[1][col]), (name, k, col)
