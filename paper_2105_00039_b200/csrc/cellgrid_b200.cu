@@ -90,7 +90,8 @@ struct cg_context {
     int cur_pos = 0, cur_attr = 0;
     // boxes
     int64_t box_cap = 0;
-    int *count = nullptr, *offset = nullptr, *mrank = nullptr, *minv = nullptr, *moff = nullptr;
+    int *count = nullptr, *offset = nullptr, *mrank = nullptr, *minv = nullptr;
+    int *count_own = nullptr;   // slab list steps: per-box ghost counts (zero between steps)
     unsigned long long *scan_status = nullptr;   // (tiles + 2) words; the last two are tickets
     int64_t scan_tiles_cap = 0;
     int table_dims[3] = {0, 0, 0};
@@ -262,7 +263,7 @@ static int ensure_boxes(cg_context *c, int64_t nb)
 {
     if (nb <= c->box_cap) return CG_OK;
     const int64_t want = nb + nb / 4 + 1024;
-    int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->moff};
+    int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->count_own};
     for (int *p : ptrs)
         if (p) cudaFree(p);
     if (c->scan_status) cudaFree(c->scan_status);
@@ -271,7 +272,8 @@ static int ensure_boxes(cg_context *c, int64_t nb)
     CUDA_TRY(c, cudaMalloc(&c->offset, sizeof(int) * (want + 1)));
     CUDA_TRY(c, cudaMalloc(&c->mrank, sizeof(int) * want));
     CUDA_TRY(c, cudaMalloc(&c->minv, sizeof(int) * want));
-    CUDA_TRY(c, cudaMalloc(&c->moff, sizeof(int) * (want + 1)));
+    CUDA_TRY(c, cudaMalloc(&c->count_own, sizeof(int) * want));
+    CUDA_TRY(c, cudaMemsetAsync(c->count_own, 0, sizeof(int) * want, c->stream));
     c->scan_tiles_cap = cdiv(want, kScanTile) + 1;
     CUDA_TRY(c, cudaMalloc(&c->scan_status, sizeof(unsigned long long) * (c->scan_tiles_cap + 2)));
     c->box_cap = want;
@@ -340,19 +342,16 @@ static Params<T> make_params(const double p[5])
     return q;
 }
 
-// Exclusive scan of the per-box counts (grid) or of the counts in Morton
-// box order (presentation).  stat may be null.
-static int launch_scan(cg_context *c, bool morton, int nb, int *out, unsigned long long *stat)
+// Exclusive scan of the per-box counts (decoupled look-back, one pass).  stat
+// may be null.
+static int launch_scan(cg_context *c, int nb, int *out, unsigned long long *stat)
 {
     const int ntiles = cdiv(nb, kScanTile);
     CUDA_TRY(c, cudaMemsetAsync(c->scan_status, 0, sizeof(unsigned long long) * ntiles, c->stream));
     unsigned *ticket = reinterpret_cast<unsigned *>(c->scan_status + c->scan_tiles_cap);
     CUDA_TRY(c, cudaMemsetAsync(ticket, 0, sizeof(unsigned), c->stream));
     ScanState S{c->scan_status, ticket};
-    if (morton)
-        scan_lookback<true><<<ntiles, kThreads, 0, c->stream>>>(nb, nullptr, c->offset, c->minv, out, S, stat);
-    else
-        scan_lookback<false><<<ntiles, kThreads, 0, c->stream>>>(nb, c->count, nullptr, nullptr, out, S, stat);
+    scan_lookback<false><<<ntiles, kThreads, 0, c->stream>>>(nb, c->count, nullptr, nullptr, out, S, stat);
     LAUNCH_CHECK(c);
     c->launches += 1;
     return CG_OK;
@@ -814,7 +813,7 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
         list_sweep_kernel<T, true><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);
         const int gb = std::min(cdiv(g.nb, kThreads), 148 * 8);
         box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);   // offsets are unused on a fused step
-        box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset, c->slots, stat);
+        box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, nullptr, c->offset, c->slots, stat);
         c->launches += 3;
     } else {
         list_sweep_kernel<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);
@@ -1423,11 +1422,20 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
     unsigned long long *stat = c->stat_dev + slot * kStatSlots;
     CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
     const int cp = c->cur_pos, ca = c->cur_attr;
-    box_keys<T><<<cdiv(nt, kThreads), kThreads, 0, st>>>(nt, g, 1.0 / g.L, (const Rec<T> *)c->b.rec[cp] - rot,
-                                                         c->count, c->b.key_rank);
-    LAUNCH_CHECK(c);
-    c->launches += 1;
-    if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
+    const bool fused = !record;   // box counting inside the list sweep (owned) + count_ghosts
+    if (!fused) {
+        box_keys<T><<<cdiv(nt, kThreads), kThreads, 0, st>>>(nt, g, 1.0 / g.L, (const Rec<T> *)c->b.rec[cp] - rot,
+                                                             c->count, c->b.key_rank);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
+    } else if (nt > no) {
+        count_ghosts<T><<<cdiv(nt - no, kThreads), kThreads, 0, st>>>(nt, rot, no, g, 1.0 / g.L,
+                                                                       (const Rec<T> *)c->b.rec[cp] - rot, c->count,
+                                                                       c->count_own);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+    }
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
     ListArgs<T> A{};
@@ -1451,12 +1459,23 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
     A.rec_m = record ? c->b.rec_m - rot : nullptr;
     A.rec_nk = record ? c->b.rec_nk - rot : nullptr;
     A.pkey = nullptr;
+    A.count = c->count;
+    A.count_own = nullptr;
+    A.invL = 1.0 / g.L;
     A.slots = c->slots;
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
     if (no > 0) {
-        list_sweep_kernel<T><<<cdiv(no, kThreads), kThreads, 0, st>>>(A);
+        if (fused) list_sweep_kernel<T, true><<<cdiv(no, kThreads), kThreads, 0, st>>>(A);
+        else list_sweep_kernel<T><<<cdiv(no, kThreads), kThreads, 0, st>>>(A);
         LAUNCH_CHECK(c);
         c->launches += 1;
+    }
+    if (fused) {
+        const int gb = std::min(cdiv(g.nb, kThreads), 148 * 8);
+        box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);
+        box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->count_own, c->offset, c->slots, stat);
+        LAUNCH_CHECK(c);
+        c->launches += 2;
     }
     finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, stat, c->bbox_dev,
                                          FINISH_COUNTERS | (freeze ? 0 : FINISH_BBOX));
@@ -1619,7 +1638,7 @@ void cg_destroy(cg_context *c)
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_agents(c);
-    int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->moff};
+    int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->count_own};
     for (int *p : ptrs)
         if (p) cudaFree(p);
     void *vptrs[] = {c->scan_status, c->slots, c->maxd_enc, c->ovf_count, c->block_counters, c->bbox_dev, c->stat_dev,
@@ -2025,7 +2044,7 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     const int slot = (int)(c->steps_done % kRing);
     unsigned long long *stat = c->stat_dev + slot * kStatSlots;
     CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
-    if ((rc = launch_scan(c, false, g.nb, c->offset, stat))) return rc;
+    if ((rc = launch_scan(c, g.nb, c->offset, stat))) return rc;
     place<<<nblk, kThreads, 0, st>>>(nn, c->b.key_rank, c->offset, c->b.tmp);
     if (c->prec == CG_FP64)
         order_gather<double, false><<<nblk, kThreads, 0, st>>>(

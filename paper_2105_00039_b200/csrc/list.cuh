@@ -41,6 +41,7 @@ struct ListArgs {
     int *rec_m, *rec_nk;      // nullptr unless recording
     int *pkey;                // this step's box (sort steps), nullptr otherwise
     int *count;               // FUSED: per-box counts accumulated here (zero on entry)
+    int *count_own;           // unused (kept zero): a slab's ghost counts come from count_ghosts
     double invL;              // FUSED: 1 / box length
     unsigned long long *slots;
     double shell_lo[3], shell_hi[3];
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kThreads) box_sum_yz(Geometry g, BoxDecode bd,
 }
 
 __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDecode bd, int *__restrict__ count,
-                                                             const int *__restrict__ syz,
+                                                             int *__restrict__ ghosts, const int *__restrict__ syz,
                                                              unsigned long long *__restrict__ slots,
                                                              unsigned long long *__restrict__ stat)
 {
@@ -259,11 +260,19 @@ __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDeco
         const int c = count[b];
         if (!c) continue;
         count[b] = 0;   // the counts start the next step at zero
+        int own = c;    // agents of b whose m is counted: a slab's ghosts are not
+        if (ghosts) {
+            const int gh = ghosts[b];
+            if (gh) {
+                own -= gh;
+                ghosts[b] = 0;
+            }
+        }
         const int ix = b / plane;
         int S = __ldg(syz + b);
         if (ix > 0) S += __ldg(syz + b - plane);
         if (ix + 1 < g.dimx) S += __ldg(syz + b + plane);
-        cand += (unsigned long long)c * (unsigned long long)(S - 1);
+        cand += (unsigned long long)own * (unsigned long long)(S - 1);
         ++occ;
         mx = max(mx, (unsigned long long)c);
     }
@@ -275,6 +284,33 @@ __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDeco
         if (cand) atomicAdd(slots + (blockIdx.x % kSlots) * kSlotWords + 7, cand);
         if (occ) atomicAdd(stat + 0, occ);
         if (mx) atomicMax(stat + 1, mx);
+    }
+}
+
+// slab list steps: the ghosts' boxes join the counts (owned agents are
+// counted inside the fused list sweep); one atomic per run of equal keys
+template <typename T>
+__global__ void __launch_bounds__(kThreads) count_ghosts(int n_total, int lo, int n_owned, Geometry g, double invL,
+                                                         const Rec<T> *__restrict__ rec, int *__restrict__ count,
+                                                         int *__restrict__ ghosts)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int ng = n_total - n_owned;
+    int flat = -1 - lane;
+    if (k < ng) {
+        const int i = k < lo ? k : k + n_owned;
+        const Rec<T> r = rec[i];
+        flat = flat_box_fast(g, invL, r.x, r.y, r.z);
+    }
+    const int prev = __shfl_up_sync(0xffffffffu, flat, 1);
+    const bool start = lane == 0 || prev != flat;
+    const unsigned starts = __ballot_sync(0xffffffffu, start);
+    const unsigned after = starts & ~(0xffffffffu >> (31 - lane));
+    const int run_end = after ? __ffs(after) - 1 : 32;
+    if (start && k < ng) {
+        atomicAdd(count + flat, run_end - lane);
+        atomicAdd(ghosts + flat, run_end - lane);
     }
 }
 
