@@ -151,6 +151,7 @@ class Context:
 
     def __init__(self, device=0, dtype=np.float64):
         lib = load()
+        self._lib = lib          # kept for close() at interpreter shutdown
         self.dtype = np.dtype(dtype)
         self.device = int(device)
         h = _P()
@@ -163,7 +164,7 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
-            load().cg_destroy(self.h)
+            self._lib.cg_destroy(self.h)
             self.h = None
 
     __del__ = close
