@@ -454,8 +454,13 @@ def main():
         torch.cuda.synchronize()
         t_e2e = reduce_max((time.perf_counter() - t0) / args.e2e_steps, world)
         es = np.dtype(pool.dtype).itemsize
+        # a sort step brings every column back (new storage order); an unsorted
+        # one only positions and displacements (engine.step)
+        sorted_steps = sum(1 for k in range(args.e2e_steps)
+                           if args.sort_every > 0 and (k + 1) % args.sort_every == 0)
+        d2h = (sorted_steps * n * (8 * es + 8) + (args.e2e_steps - sorted_steps) * n * 6 * es) // args.e2e_steps
         e2e = {"value": n * world / t_e2e, "unit": UNIT,
-               "h2d_bytes_per_step": n * (5 * es + 8), "d2h_bytes_per_step": n * (8 * es + 8),
+               "h2d_bytes_per_step": n * (5 * es + 8), "d2h_bytes_per_step": d2h,
                "ms_per_step": t_e2e * 1e3, "api": "engine.step(pool, SimulationConfig(strategy=Gpu()))"}
 
     cpu = None

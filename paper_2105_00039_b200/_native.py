@@ -204,13 +204,17 @@ class Context:
         check(load().cg_download(self.h, *args), self.h)
         return out
 
-    def step_download(self, params5, interaction_radius=None, box_cap=1 << 24, flags=0, into=None):
+    def step_download(self, params5, interaction_radius=None, box_cap=1 << 24, flags=0, into=None,
+                      columns=("px", "py", "pz", "diameter", "adherence", "uid", "dx", "dy", "dz")):
         """step + download with the unchanged columns copied during the sweep
-        (cg_step_download); returns (stats, columns)."""
+        (cg_step_download); returns (stats, the requested columns)."""
         p = np.ascontiguousarray(params5, np.float64)
         ir = float("nan") if interaction_radius is None else float(interaction_radius)
         out, args = {}, []
         for name in ("px", "py", "pz", "diameter", "adherence", "uid", "dx", "dy", "dz"):
+            if name not in columns:
+                args.append(None)
+                continue
             dst = None if into is None else into.get(name)
             if dst is None or dst.shape[0] != self.n:
                 dst = np.empty(self.n, np.uint64 if name == "uid" else self.dtype)

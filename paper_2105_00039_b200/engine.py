@@ -269,6 +269,7 @@ def _upload(ctx, pool):
                pool.adherence, pool.uid)
 
 
+_POOL_KEYS = ("px", "py", "pz", "diameter", "adherence", "uid", "dx", "dy", "dz")
 _POOL_COLS = (("px", "position_x"), ("py", "position_y"), ("pz", "position_z"),
               ("diameter", "diameter"), ("adherence", "adherence"), ("uid", "uid"),
               ("dx", "displacement_x"), ("dy", "displacement_y"), ("dz", "displacement_z"))
@@ -334,9 +335,16 @@ def step(pool, config: SimulationConfig, step_index=0):
         return st
     ctx = _context(config.strategy, pool.dtype)
     _upload(ctx, pool)
-    # the step and the download of its result, transfers overlapped with the sweep
+    # the step and the download of its result, transfers overlapped with the sweep;
+    # a step without the Z-order sort keeps the storage order, so diameter,
+    # adherence and uid on the host are already the device's
+    flags = step_flags(config, step_index)
+    sorted_step = bool(flags & _native.CG_STEP_SORT)
+    wanted = _POOL_KEYS if sorted_step else ("px", "py", "pz", "dx", "dy", "dz")
     st, cols = ctx.step_download(params_vector(config.force_params), config.interaction_radius,
-                                 DEFAULT_BOX_CAP, step_flags(config, step_index), into=_reusable(ctx, pool))
+                                 DEFAULT_BOX_CAP, flags, into=_reusable(ctx, pool), columns=wanted)
+    if not sorted_step:
+        cols.update(diameter=pool.diameter, adherence=pool.adherence, uid=pool.uid)
     _assign(pool, cols)
     out = _to_stats(st, step_index, pool.precision.itemsize)
     out.divisions = divisions
