@@ -35,6 +35,9 @@
 
 #include "../../include/cellgrid_b200.h"
 
+#ifndef CG_LIST_BUILD_MINB
+#define CG_LIST_BUILD_MINB 4   // the same sweep building neighbour lists
+#endif
 #ifndef CG_SPARSE_MINB
 #define CG_SPARSE_MINB 4   // resident 256-thread CTAs per SM for the sparse sweep (measured)
 #endif
@@ -563,7 +566,7 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
     if (!c->last_dense && A.nbr) {   // sparse sweep that also builds the neighbour lists
         cudaStream_t st = c->stream;
         CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
-        sweep7_kernel<T, true, false, 16, false, CG_SPARSE_MINB, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
+        sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
         sweep7_overflow<T, true, false, 16, true><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
         LAUNCH_CHECK(c);
         c->launches += 2;
