@@ -813,13 +813,13 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     A.slots = c->slots;
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
     if (fused) {
-        list_sweep_kernel<T, true><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);
+        list_sweep_kernel<T, true><<<cdiv(n, kListThreads), kListThreads, 0, st>>>(A);
         const int gb = std::min(cdiv(g.nb, kThreads), 148 * 8);
         box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);   // offsets are unused on a fused step
         box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, nullptr, c->offset, c->slots, stat);
         c->launches += 3;
     } else {
-        list_sweep_kernel<T><<<cdiv(n, kThreads), kThreads, 0, st>>>(A);
+        list_sweep_kernel<T><<<cdiv(n, kListThreads), kListThreads, 0, st>>>(A);
         c->launches += 1;
     }
     finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, stat, c->bbox_dev,
@@ -1468,8 +1468,8 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
     A.slots = c->slots;
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
     if (no > 0) {
-        if (fused) list_sweep_kernel<T, true><<<cdiv(no, kThreads), kThreads, 0, st>>>(A);
-        else list_sweep_kernel<T><<<cdiv(no, kThreads), kThreads, 0, st>>>(A);
+        if (fused) list_sweep_kernel<T, true><<<cdiv(no, kListThreads), kListThreads, 0, st>>>(A);
+        else list_sweep_kernel<T><<<cdiv(no, kListThreads), kListThreads, 0, st>>>(A);
         LAUNCH_CHECK(c);
         c->launches += 1;
     }

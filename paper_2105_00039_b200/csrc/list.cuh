@@ -63,6 +63,10 @@ __device__ __noinline__ void degenerate_pair(uint64_t ui, uint64_t uj, T mag, T 
 #ifndef CG_LIST_AHEAD
 #define CG_LIST_AHEAD 1
 #endif
+#ifndef CG_LIST_THREADS
+#define CG_LIST_THREADS 256
+#endif
+constexpr int kListThreads = CG_LIST_THREADS;
 #ifndef CG_LIST_MINB
 #define CG_LIST_MINB 4
 #endif
@@ -72,7 +76,7 @@ __device__ __noinline__ void degenerate_pair(uint64_t ui, uint64_t uj, T mag, T 
 // separate box_keys pass; m and the grid statistics then come from the
 // per-box pass box_stencil_pass (a step without CG_STEP_RECORD).
 template <typename T, bool FUSED = false>
-__global__ void __launch_bounds__(kThreads, CG_LIST_MINB) list_sweep_kernel(ListArgs<T> A)
+__global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(ListArgs<T> A)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int a = A.own_lo + t;
