@@ -60,9 +60,6 @@ __device__ __noinline__ void degenerate_pair(uint64_t ui, uint64_t uj, T mag, T 
     fz = fz + (T)((double)mag * (sign * uz));
 }
 
-#ifndef CG_LIST_AHEAD
-#define CG_LIST_AHEAD 1
-#endif
 #ifndef CG_LIST_THREADS
 #define CG_LIST_THREADS 256
 #endif
@@ -130,24 +127,6 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
         T last_rj = T(-1), last_req = zero;
         const int cnt = A.nbr_n[a];
         const int *L = A.nbr + a;
-#if CG_LIST_AHEAD == 2
-        // three indices and two records ahead of the pair being evaluated
-        int j1 = cnt > 0 ? __ldg(L) : 0;
-        int j2 = cnt > 1 ? __ldg(L + A.nbr_stride) : 0;
-        int j3 = cnt > 2 ? __ldg(L + 2 * A.nbr_stride) : 0;
-        Rec<T> o1, o2;
-        if (cnt > 0) o1 = A.rec[j1];
-        if (cnt > 1) o2 = A.rec[j2];
-#pragma unroll 1
-        for (int p = 0; p < cnt; ++p) {
-            const int jc = j1;
-            const Rec<T> co = o1;
-            j1 = j2;
-            o1 = o2;
-            j2 = j3;
-            if (p + 2 < cnt) o2 = A.rec[j2];
-            if (p + 3 < cnt) j3 = __ldg(L + (p + 3) * A.nbr_stride);
-#else
         // two indices and one record ahead of the pair being evaluated
         int jn = cnt > 0 ? __ldg(L) : 0;
         int jnn = cnt > 1 ? __ldg(L + A.nbr_stride) : 0;
@@ -160,7 +139,6 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
             jn = jnn;
             if (p + 1 < cnt) o = A.rec[jn];
             if (p + 2 < cnt) jnn = __ldg(L + (p + 2) * A.nbr_stride);
-#endif
             // the reference's pass-1 test and pass-2 expressions (kernels.py:198-257)
             const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;
             const T rj = co.d * half;
