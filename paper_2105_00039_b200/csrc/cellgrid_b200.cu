@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1607,6 +1608,12 @@ int cg_create(int device, int precision, cg_context **out)
     c->device = device;
     c->prec = precision;
     c->esz = precision == CG_FP64 ? 8 : 4;
+    // test hook: CG_LIST_SKIN_DEFAULT (same units as CG_OPT_LIST_SKIN) sets the
+    // initial neighbour-list skin of every new context
+    if (const char *e = std::getenv("CG_LIST_SKIN_DEFAULT")) {
+        const int v = std::atoi(e);
+        c->list_skin = v < 0 ? -1.0 : v * 1e-3;
+    }
     int rc = CG_OK;
     auto chk = [&](cudaError_t e) {
         if (e != cudaSuccess && rc == CG_OK) rc = fail(c, CG_ERR_CUDA, "%s", cudaGetErrorString(e));

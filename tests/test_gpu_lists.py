@@ -96,6 +96,7 @@ def test_lists_match_oracle(cuda_required):
     ref = pool.copy()
     ctx = N.Context(0, pool.dtype)
     ctx.set_option(N.CG_OPT_SUMMATION, 0)
+    ctx.set_option(N.CG_OPT_LIST_SKIN, -1)
     ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
     for k in range(6):
         st = ctx.step(PARAMS5, None, 1 << 24, N.CG_STEP_SORT)
