@@ -15,12 +15,12 @@ pytestmark = pytest.mark.gpu
 PARAMS5 = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
 
 
-def _pool():
-    from paper_2105_00039_b200.pool import AgentPool
+def _pool(fp32=False):
+    from paper_2105_00039_b200.pool import AgentPool, PrecisionMode
     from paper_2105_00039_b200.workloads import jittered_lattice_positions
     pos = jittered_lattice_positions(20, spacing=7.0, jitter=1.0, seed=5)
     pos[:, 0] *= 1.4
-    return AgentPool.from_arrays(pos, 10.0, 0.4)
+    return AgentPool.from_arrays(pos, 10.0, 0.4, PrecisionMode.FP32 if fp32 else PrecisionMode.FP64)
 
 
 def _free_port():
@@ -31,7 +31,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1):
+def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1, fp32=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -41,7 +41,7 @@ def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1):
     from paper_2105_00039_b200.distributed import SlabRunner, TorchExchange
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % port, rank=rank, world_size=world)
-    full = _pool()
+    full = _pool(fp32)
     mine = (full.uid % world) == rank            # ignores the slab rule: step 1 migrates
     ctx = _native.Context(0, full.dtype)
     ctx.set_option(_native.CG_OPT_SUMMATION, summation)
@@ -62,7 +62,8 @@ def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1):
 @pytest.mark.parametrize("world,summation,skin,params", [
     (2, 0, 0, (2.0, 1.0, 0.01, 3.0, 1.0)), (3, 1, 0, (2.0, 1.0, 0.01, 3.0, 1.0)),
     (2, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)), (3, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)),
-    (5, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0))])   # 5 slabs of ~4 planes: ghost bands reach two ranks away
+    (5, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)),    # 5 slabs of ~4 planes: ghost bands reach two ranks away
+    (3, 0, -2, (2.0, 1.0, 0.002, 3.0, 1.0))])   # skin -2: lists on, fp32 pool
 def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, params):
     """skin 0: a full exchange every step; skin -1: neighbour lists, the
     partition frozen and the ghosts refreshed between rebuilds (small
@@ -74,7 +75,9 @@ def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, 
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
     port = _free_port()
-    procs = [mpc.Process(target=_worker, args=(r, world, port, steps, PARAMS5, summation, q, skin))
+    fp32 = skin == -2
+    skin = -1 if fp32 else skin
+    procs = [mpc.Process(target=_worker, args=(r, world, port, steps, PARAMS5, summation, q, skin, fp32))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -83,7 +86,7 @@ def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, 
         p.join(timeout=120)
         assert p.exitcode == 0
     # single-context run of the global pool
-    full = _pool()
+    full = _pool(fp32)
     ctx = _native.Context(0, full.dtype)
     ctx.set_option(_native.CG_OPT_SUMMATION, summation)
     ctx.upload(full.position_x, full.position_y, full.position_z, full.diameter, full.adherence, full.uid)
