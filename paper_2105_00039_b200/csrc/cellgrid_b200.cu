@@ -57,7 +57,8 @@ namespace {
 
 constexpr int kStatSlots = 8;        // per step: occupied, maxocc, evals, cands, ndeg
 constexpr int kRing = 64;            // pinned stats ring (steps in flight)
-constexpr int kBboxBlocks = 148 * 4;
+// grid-stride launches are sized in multiples of the SM count (cg_create
+// reads it; 148 on a B200)
 constexpr int kMaxCounterBlocks = 1 << 20;
 
 enum { PRES_IDENTITY = 0, PRES_VALID = 1, PRES_PENDING = 2 };
@@ -85,6 +86,7 @@ struct Buffers {
 
 struct cg_context {
     int device = 0;
+    int sms = 148;                // streaming multiprocessors of the device
     int prec = CG_FP64;
     size_t esz = 8;
     cudaStream_t stream = nullptr;
@@ -381,7 +383,7 @@ static int standalone_bbox(cg_context *c)
 {
     const int n = (int)c->n_owned;
     cudaStream_t st = c->stream;
-    bbox_slots<T><<<std::min(kBboxBlocks, cdiv(n, kThreads)), kThreads, 0, st>>>(
+    bbox_slots<T><<<std::min(c->sms * 4, cdiv(n, kThreads)), kThreads, 0, st>>>(
         n, (const Rec<T> *)c->b.rec[c->cur_pos], c->slots);
     finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, nullptr, c->bbox_dev, FINISH_BBOX);
     LAUNCH_CHECK(c);
@@ -403,7 +405,7 @@ static int materialize_presentation(cg_context *c, cudaStream_t st = nullptr)
     if (c->table_dims[0] != g.dimx || c->table_dims[1] != g.dimy || c->table_dims[2] != g.dimz) {
         int rc = ensure_boxes(c, g.nb);
         if (rc) return rc;
-        morton_table<<<std::min(cdiv(g.nb, kThreads), 148 * 16), kThreads, 0, st>>>(g, c->mrank, c->minv);
+        morton_table<<<std::min(cdiv(g.nb, kThreads), c->sms * 16), kThreads, 0, st>>>(g, c->mrank, c->minv);
         LAUNCH_CHECK(c);
         c->launches += 1;
         c->table_dims[0] = g.dimx;
@@ -554,7 +556,7 @@ static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
     LAUNCH_CHECK(c);
     c->launches += 1;
     if (!FLUSH) {   // agents with more than KS survivors (none in most steps)
-        sweep7_overflow<T, UID, ZS, KS><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
+        sweep7_overflow<T, UID, ZS, KS><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
         LAUNCH_CHECK(c);
         c->launches += 1;
     }
@@ -568,7 +570,7 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         cudaStream_t st = c->stream;
         CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
         sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
-        sweep7_overflow<T, true, false, 16, true><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
+        sweep7_overflow<T, true, false, 16, true><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
         LAUNCH_CHECK(c);
         c->launches += 2;
         return CG_OK;
@@ -588,7 +590,7 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
     // dense: one warp per agent (warp-cooperative walk, survivors compacted
     // into a per-warp queue); uid order bit-exact, stencil order deterministic
     cudaStream_t st = c->stream;
-    const int blocks = std::min(cdiv(A.n, kThreads / 32), 148 * 16);
+    const int blocks = std::min(cdiv(A.n, kThreads / 32), c->sms * 16);
     CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
     if (c->summation == SUM_UID) {
         auto k = sweep_warp_kernel<T, true>;
@@ -596,7 +598,7 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         CUDA_TRY(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k<<<blocks, kThreads, sm, st>>>(A);
         LAUNCH_CHECK(c);
-        sweep7_overflow<T, true, true, 16><<<std::min(cdiv(A.n, kThreads), 148 * 2), kThreads, 0, st>>>(A);
+        sweep7_overflow<T, true, true, 16><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
         LAUNCH_CHECK(c);
         c->launches += 2;
     } else {
@@ -815,7 +817,7 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
     if (fused) {
         list_sweep_kernel<T, true><<<cdiv(n, kListThreads), kListThreads, 0, st>>>(A);
-        const int gb = std::min(cdiv(g.nb, kThreads), 148 * 8);
+        const int gb = std::min(cdiv(g.nb, kThreads), c->sms * 8);
         box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);   // offsets are unused on a fused step
         box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, nullptr, c->offset, c->slots, stat);
         c->launches += 3;
@@ -1208,7 +1210,7 @@ static int slab_plan_t(cg_context *c, const double bb[9], double ir, int64_t box
     CUDA_TRY(c, cudaMemsetAsync(S.counts, 0, sizeof(unsigned long long) * kHist, st));
     const int n = (int)c->n_owned;
     if (n > 0) {
-        slab_dest<T><<<std::min(cdiv(n, kThreads), 148 * 8), kThreads, 0, st>>>(
+        slab_dest<T><<<std::min(cdiv(n, kThreads), c->sms * 8), kThreads, 0, st>>>(
             n, g, S.B, rank, (const Rec<T> *)c->b.rec[c->cur_pos], S.dest, S.counts);
         LAUNCH_CHECK(c);
         c->launches += 1;
@@ -1475,7 +1477,7 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
         c->launches += 1;
     }
     if (fused) {
-        const int gb = std::min(cdiv(g.nb, kThreads), 148 * 8);
+        const int gb = std::min(cdiv(g.nb, kThreads), c->sms * 8);
         box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);
         box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->count_own, c->offset, c->slots, stat);
         LAUNCH_CHECK(c);
@@ -1606,6 +1608,7 @@ int cg_create(int device, int precision, cg_context **out)
     if (cudaSetDevice(device) != cudaSuccess) return CG_ERR_NO_DEVICE;
     cg_context *c = new cg_context();
     c->device = device;
+    c->sms = prop.multiProcessorCount;
     c->prec = precision;
     c->esz = precision == CG_FP64 ? 8 : 4;
     // test hook: CG_LIST_SKIN_DEFAULT (same units as CG_OPT_LIST_SKIN) sets the
@@ -1773,12 +1776,12 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
     CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, sizeof(unsigned long long), st));
     if (!c->maxuid_dev) CUDA_TRY(c, cudaMalloc(&c->maxuid_dev, sizeof(unsigned long long)));
     CUDA_TRY(c, cudaMemsetAsync(c->maxuid_dev, 0, sizeof(unsigned long long), st));
-    max_uid_kernel<<<std::min(kBboxBlocks, nblk), kThreads, 0, st>>>((int)n, c->b.uid[0], c->maxuid_dev);
+    max_uid_kernel<<<std::min(c->sms * 4, nblk), kThreads, 0, st>>>((int)n, c->b.uid[0], c->maxuid_dev);
     if (c->prec == CG_FP64)
-        max_diam_kernel<double><<<std::min(kBboxBlocks, nblk), kThreads, 0, st>>>(
+        max_diam_kernel<double><<<std::min(c->sms * 4, nblk), kThreads, 0, st>>>(
             (int)n, (const Rec<double> *)c->b.rec[0], c->maxd_enc);
     else
-        max_diam_kernel<float><<<std::min(kBboxBlocks, nblk), kThreads, 0, st>>>(
+        max_diam_kernel<float><<<std::min(c->sms * 4, nblk), kThreads, 0, st>>>(
             (int)n, (const Rec<float> *)c->b.rec[0], c->maxd_enc);
     LAUNCH_CHECK(c);
     c->launches += 3;
