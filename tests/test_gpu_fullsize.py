@@ -92,3 +92,24 @@ def test_c4_lists_deterministic_and_sort_invariant(cuda_required, c4):
         out.append({k: v[o] for k, v in cols.items()})
     for col in out[0]:
         assert np.array_equal(out[0][col], out[1][col]), col
+
+
+def test_c4_long_run_lists_change_nothing(cuda_required, c4):
+    """300 resident C4 steps (dozens of list epochs): every step's counters and
+    the final pool are identical with and without neighbour lists."""
+    from paper_2105_00039_b200 import _native as N
+    runs = []
+    for skin in (-1, 0):
+        ctx = _ctx(c4, skin)
+        try:
+            ids = [ctx.step(PARAMS5, None, 1 << 24, N.CG_STEP_SORT, wait=False) for _ in range(300)]
+            ctx.synchronize()
+            counters = [(s.force_evals, s.candidates, s.degenerate_pairs, s.grid_occupied_boxes,
+                         s.grid_max_occupancy) for s in (ctx.fetch_stats(i) for i in ids[-60:])]
+            runs.append((counters, ctx.download(), ctx.list_stats()))
+        finally:
+            ctx.close()
+    assert runs[0][2]["builds"] >= 10 and runs[0][2]["list_steps"] >= 200, runs[0][2]
+    assert runs[0][0] == runs[1][0]
+    for col in runs[0][1]:
+        assert np.array_equal(runs[0][1][col], runs[1][1][col]), col
