@@ -25,6 +25,13 @@ def c4():
     return workloads.c4()
 
 
+@pytest.fixture(scope="module")
+def c4f():
+    from paper_2105_00039_b200 import workloads
+    from paper_2105_00039_b200.pool import PrecisionMode
+    return workloads.c4(PrecisionMode.FP32)
+
+
 def _ctx(pool, skin=-1):
     from paper_2105_00039_b200 import _native as N
     ctx = N.Context(0, pool.dtype)
@@ -94,13 +101,15 @@ def test_c4_lists_deterministic_and_sort_invariant(cuda_required, c4):
         assert np.array_equal(out[0][col], out[1][col]), col
 
 
-def test_c4_long_run_lists_change_nothing(cuda_required, c4):
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_c4_long_run_lists_change_nothing(cuda_required, c4, c4f, prec):
     """300 resident C4 steps (dozens of list epochs): every step's counters and
     the final pool are identical with and without neighbour lists."""
     from paper_2105_00039_b200 import _native as N
+    pool = c4 if prec == "fp64" else c4f
     runs = []
     for skin in (-1, 0):
-        ctx = _ctx(c4, skin)
+        ctx = _ctx(pool, skin)
         try:
             ids = [ctx.step(PARAMS5, None, 1 << 24, N.CG_STEP_SORT, wait=False) for _ in range(300)]
             ctx.synchronize()

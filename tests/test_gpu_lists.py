@@ -206,3 +206,35 @@ def test_fused_list_steps_change_nothing(cuda_required, name, pool):
         assert a[0] == b[0], (name, k)
         for col in a[1]:
             assert np.array_equal(a[1][col], b[1][col]), (name, k, col)
+
+
+@pytest.mark.parametrize("spacing,ir", [(8.0, 11.0), (10.0, 12.5)])
+def test_lists_with_interaction_radius(cuda_required, spacing, ir):
+    """interaction_radius above the diameter: larger boxes (L = ir) and a skin
+    of 0.07 L (still on the sparse path, where lists apply); list steps equal
+    list-free steps and the oracle."""
+    from paper_2105_00039_b200 import _native as N
+    from paper_2105_00039_b200.mechanics import ForceParams
+    from paper_2105_00039_b200.pool import AgentPool
+    from paper_2105_00039_b200.workloads import jittered_lattice_positions
+    pool = AgentPool.from_arrays(jittered_lattice_positions(24, spacing, 1.0, 21), 10.0, 0.4)
+    outs = []
+    for skin in (-1, 0):
+        ctx = N.Context(0, pool.dtype)
+        ctx.set_option(N.CG_OPT_SUMMATION, 0)
+        ctx.set_option(N.CG_OPT_LIST_SKIN, skin)
+        ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+        sts = [ctx.step(PARAMS5, ir, 1 << 24, N.CG_STEP_SORT) for _ in range(12)]
+        outs.append(([(s.force_evals, s.candidates, s.grid_occupied_boxes) for s in sts], ctx.download(),
+                     ctx.list_stats()))
+        ctx.close()
+    assert outs[0][2]["list_steps"] > 0
+    ref = pool.copy()
+    ref_c = []
+    for _ in range(12):
+        r = oracle.step(ref, ForceParams(), sort=True, interaction_radius=ir, threads=8)
+        ref_c.append((r.force_evals, r.candidates, int(np.count_nonzero(r.box_count))))
+    assert outs[0][0] == outs[1][0] == ref_c
+    for cols in (outs[0][1], outs[1][1]):
+        assert np.array_equal(cols["uid"], ref.uid)
+        assert np.array_equal(cols["px"], ref.position_x) and np.array_equal(cols["dz"], ref.displacement_z)
