@@ -137,6 +137,8 @@ struct cg_context {
     double list_skin = -1.0;
     int *nbr = nullptr, *nbr_n = nullptr;
     int64_t nbr_cap = 0;
+    int nbr_width = 0;            // entries per agent allocated
+    int list_width = kListCap;    // entries per agent of the current lists
     bool list_valid = false;      // lists cover every pair that can overlap now
     int last_kind = 0;            // previous step: 0 other, 1 list build, 2 list step
     bool last_freeze = false;
@@ -566,11 +568,18 @@ static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
 template <typename T>
 static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
 {
-    if (!c->last_dense && A.nbr) {   // sparse sweep that also builds the neighbour lists
+    if (A.nbr) {   // grid sweep that also builds the neighbour lists (uid order)
         cudaStream_t st = c->stream;
         CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
-        sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
-        sweep7_overflow<T, true, false, 16, true><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
+        if (!c->last_dense) {
+            sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
+            sweep7_overflow<T, true, false, 16, true><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
+        } else {
+            // dense: z-sorted boxes cut each column run; most agents have more
+            // than 16 partners and take the overflow kernel's rounds
+            sweep7_kernel<T, true, true, 16, false, 3, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
+            sweep7_overflow<T, true, true, 16, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
+        }
         LAUNCH_CHECK(c);
         c->launches += 2;
         return CG_OK;
@@ -705,10 +714,11 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     A.n_owned = (int)c->n_owned;
     A.own_lo = c->rot;
     A.uid32 = c->uid32;
-    if (build_lists && !c->last_dense) {
+    if (build_lists) {
         A.nbr = c->nbr;
         A.nbr_n = c->nbr_n;
         A.nbr_stride = c->nbr_cap;
+        A.list_cap = c->list_width;
         A.skin = (T)c->list_skin_used;
         A.skin_f = nextafterf((float)c->list_skin_used, INFINITY);
     }
@@ -722,22 +732,46 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     c->launches += 1;
     if (!freeze)
         CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host, c->bbox_dev, 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    else   // frozen: the bbox is unchanged, but a list build's overflow count is new
+        CUDA_TRY(c, cudaMemcpyAsync(c->bbox_host + 7, c->bbox_dev + 7, 2 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
     c->bbox_valid = true;
     return CG_OK;
 }
 
 // ---------------------------------------------------------------- neighbour-list reuse
-static int ensure_lists(cg_context *c)
+static int ensure_lists(cg_context *c, int width = kListCap)
 {
-    if (c->nbr && c->nbr_cap == c->cap) return CG_OK;
+    if (c->nbr && c->nbr_cap == c->cap && c->nbr_width >= width) return CG_OK;
     if (c->nbr) cudaFree(c->nbr);
     if (c->nbr_n) cudaFree(c->nbr_n);
     c->nbr = c->nbr_n = nullptr;
     c->nbr_cap = 0;
-    CUDA_TRY(c, cudaMalloc(&c->nbr, sizeof(int) * (size_t)kListCap * (size_t)c->cap));
+    c->nbr_width = 0;
+    CUDA_TRY(c, cudaMalloc(&c->nbr, sizeof(int) * (size_t)width * (size_t)c->cap));
     CUDA_TRY(c, cudaMalloc(&c->nbr_n, sizeof(int) * (size_t)c->cap));
     c->nbr_cap = c->cap;
+    c->nbr_width = width;
     return CG_OK;
+}
+
+// list width for the next build: kListCap on sparse pools; on dense pools
+// (the same test as build_grid_geo) the expected partner count within
+// max diameter + skin at the pool's mean density (bbox volume) plus a Poisson
+// tail; 0 = too wide, no lists.  An agent with more partners than the width
+// still makes the build's lists unusable (overflow count), never wrong.
+static int list_width_for(const cg_context *c, const Geometry &g, double skin)
+{
+    const double surv = 4.19 * (double)c->n / (double)g.nb;
+    const bool dense = c->path == 2 || (c->path == 0 && surv > 10.0);
+    if (!dense) return kListCap;
+    double vol = 1.0;
+    for (int q = 0; q < 3; ++q) vol *= std::max(c->bbox_host[3 + q] - c->bbox_host[q], g.L);
+    const double r = c->max_diam + skin;
+    const double mu = 4.18879 * r * r * r * (double)c->n / vol;
+    const int w = ((int)std::ceil(1.25 * mu + 6.0 * std::sqrt(mu) + 16.0) + 15) & ~15;
+    if (w > 512 || (double)w * (double)c->cap * 4.0 > 8e9) return 0;
+    return std::max(w, kListCap);
 }
 
 // After the previous step's readback: lists built last step become valid if
@@ -976,9 +1010,16 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
         bool build = lists_on && c->list_wait == 0;
         if (c->list_wait > 0) c->list_wait--;
         if (build) {
-            if ((rc = ensure_lists(c))) return rc;
             c->list_skin_used = c->list_skin < 0 ? 0.07 * g.L : c->list_skin;
             build = c->list_skin_used > 0 && c->list_skin_used <= g.L;
+            c->list_width = build ? list_width_for(c, g, c->list_skin_used) : 0;
+            build = build && c->list_width > 0;
+            // dense pools: no build while the last moving grid sweep moved some
+            // agent by more than skin / 4 (the lists would not serve 2 steps)
+            if (build && c->list_width != kListCap && !freeze && c->last_kind == 0 && !c->last_freeze &&
+                4.0 * std::sqrt(std::max(c->bbox_host[7], 0.0)) > c->list_skin_used)
+                build = false;
+            if (build && (rc = ensure_lists(c, c->list_width))) return rc;
         }
         if ((rc = build_grid_geo<T>(c, g, relayout, sort))) return rc;
         CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
@@ -989,7 +1030,6 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
             c->pres_state = PRES_PENDING;
         }
         if (c->early.want && (rc = early_download<T>(c))) return rc;
-        build = build && !c->last_dense;
         c->list_valid = false;
         if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
         c->last_kind = build ? 1 : 0;
@@ -1541,6 +1581,7 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
             if (c->list_wait > 0) c->list_wait--;
             if (build) {
                 if ((rc = ensure_lists(c))) return rc;
+                c->list_width = kListCap;
                 c->list_skin_used = c->list_skin < 0 ? 0.07 * S.g.L : c->list_skin;
                 build = c->list_skin_used > 0 && c->list_skin_used <= S.g.L;
             }

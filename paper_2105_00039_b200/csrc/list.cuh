@@ -33,7 +33,7 @@ struct ListArgs {
     const T *adh;
     const uint64_t *uid;
     Params<T> p;
-    const int *nbr;           // [kListCap][nbr_stride]
+    const int *nbr;           // [list width][nbr_stride]
     const int *nbr_n;
     long long nbr_stride;
     T *disp_x, *disp_y, *disp_z;

@@ -62,14 +62,15 @@ struct Sweep7Args {
     int own_lo;                 // targets are storage indices [own_lo, own_lo + n_owned): a relaid
                                 // slab sub-grid keeps its lo ghosts in front of the owned agents
     // neighbour lists (LIST builds): partners within ri + rj + skin, uid order
-    int *nbr;                   // [kListCap][nbr_stride] storage indices
+    int *nbr;                   // [list_cap][nbr_stride] storage indices
     int *nbr_n;                 // per storage index
     long long nbr_stride;
     T skin;
     float skin_f;               // skin rounded up, for the prefilter reach
+    int list_cap;               // list entries per agent (more: the list set is not used)
 };
 
-constexpr int kListCap = 48;    // list entries per agent (more: the list set is not used)
+constexpr int kListCap = 48;    // list width of sparse pools (dense pools: sized from the density)
 
 // slot -> storage index: the idx map, or the slot itself (relaid storage)
 template <typename A_t>
@@ -263,7 +264,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 const T dist = tsqrt<T>(dx * dx + dy * dy + dz * dz);
                 const T rsum = ri + rj;
                 if (LIST && dist <= rsum + A.skin) {
-                    if (nl < kListCap) A.nbr[nl * A.nbr_stride + a] = jc;
+                    if (nl < A.list_cap) A.nbr[nl * A.nbr_stride + a] = jc;
                     ++nl;
                 }
                 const T delta = rsum - dist;
@@ -410,9 +411,10 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         A.disp_z[a] = ddz;
         if (LIST) {
             A.nbr_n[a] = nl;
-            if (nl > kListCap) atomicAdd(A.slots + (blockIdx.x % kSlots) * kSlotWords + 10, 1ull);
-            dmax2 = fmaxf(dmax2, (float)((double)ddx * ddx + (double)ddy * ddy + (double)ddz * ddz));
+            if (nl > A.list_cap) atomicAdd(A.slots + (blockIdx.x % kSlots) * kSlotWords + 10, 1ull);
         }
+        if (LIST || ZSORTED)   // the step's largest displacement (list validity / build decision)
+            dmax2 = fmaxf(dmax2, (float)((double)ddx * ddx + (double)ddy * ddy + (double)ddz * ddz));
         if (A.new_rec) {               // engine.py:325-327 (separate buffer: two-phase)
             const T nxp = xi + ddx, nyp = yi + ddy, nzp = zi + ddz;
             Rec<T> nr;
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, MINB) sweep7_kernel(Sweep7Args<T> A)
     float dmax2 = 0.f;
     if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true, LIST>(A, s, c_m, c_nk, c_nd, dmax2);
     warp_counters(A.slots, c_m, c_nk, c_nd);
-    if (LIST) warp_dmax(A.slots, dmax2);
+    if (LIST || ZSORTED) warp_dmax(A.slots, dmax2);
 }
 
 // agents deferred by sweep7_kernel (more than KS survivors): grid-stride over
@@ -490,7 +492,7 @@ __global__ void __launch_bounds__(kThreads) sweep7_overflow(Sweep7Args<T> A)
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
         sweep_agent<T, UIDMODE, ZSORTED, KS, false, false, LIST>(A, A.ovf[k], c_m, c_nk, c_nd, dmax2);
     warp_counters(A.slots, c_m, c_nk, c_nd);
-    if (LIST) warp_dmax(A.slots, dmax2);
+    if (LIST || ZSORTED) warp_dmax(A.slots, dmax2);
 }
 
 }  // namespace cg

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
     int *Q = S.q[wid];
     const unsigned lt = (1u << lane) - 1u;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
+    float dmax2 = 0.f;
     const float Lf = (float)A.g.L;
     const T zero = A.p.zero;
     for (int s = blockIdx.x * (kThreads / 32) + wid; s < A.n; s += gridDim.x * (kThreads / 32)) {
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
             A.disp_x[a] = ddx;
             A.disp_y[a] = ddy;
             A.disp_z[a] = ddz;
+            dmax2 = fmaxf(dmax2, (float)((double)ddx * ddx + (double)ddy * ddy + (double)ddz * ddz));
             if (A.new_rec) {
                 Rec<T> nr;
                 nr.x = me.x + ddx;
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
         __syncwarp();
     }
     warp_counters(A.slots, c_m, c_nk, c_nd);
+    warp_dmax(A.slots, dmax2);   // the step's largest displacement (list-build decision)
 }
 
 }  // namespace cg

@@ -238,3 +238,60 @@ def test_lists_with_interaction_radius(cuda_required, spacing, ir):
     for cols in (outs[0][1], outs[1][1]):
         assert np.array_equal(cols["uid"], ref.uid)
         assert np.array_equal(cols["px"], ref.position_x) and np.array_equal(cols["dz"], ref.displacement_z)
+
+
+def _dense_pool(n, density, seed):
+    from paper_2105_00039_b200.geometry import Aabb
+    from paper_2105_00039_b200.pool import AgentPool
+    from paper_2105_00039_b200.workloads import box_side_for_density
+    return AgentPool.spawn_random(n, Aabb.cube(box_side_for_density(n, 10.0, density)), 10.0, 0.4, seed)
+
+
+@pytest.mark.parametrize("density", [27.0, 100.0])
+def test_dense_lists_match_oracle(cuda_required, density):
+    """Dense pools (the z-sorted-box path): lists sized from the density are
+    built by the grid sweep and serve frozen steps (benchmark B) and then
+    moving steps; every step equals the C oracle bit for bit in uid order."""
+    from paper_2105_00039_b200 import _native as N
+    from paper_2105_00039_b200.mechanics import ForceParams
+    pool = _dense_pool(12000, density, 5)
+    ref = pool.copy()
+    ctx = N.Context(0, pool.dtype)
+    ctx.set_option(N.CG_OPT_SUMMATION, 0)
+    ctx.set_option(N.CG_OPT_LIST_SKIN, -1)
+    ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+    kinds = []
+    for k in range(10):
+        freeze = k < 6
+        st = ctx.step(PARAMS5, None, 1 << 24, N.CG_STEP_SORT | (N.CG_STEP_FREEZE if freeze else 0))
+        kinds.append(int(st.sweep_kind))
+        r = oracle.step(ref, ForceParams(), sort=True, freeze=freeze, threads=8)
+        assert (st.force_evals, st.candidates, st.degenerate_pairs, st.grid_max_occupancy) == (
+            r.force_evals, r.candidates, r.degenerate_pairs, int(r.box_count.max())), k
+        cols = ctx.download()
+        assert np.array_equal(cols["uid"], ref.uid)
+        for a, b in (("px", "position_x"), ("py", "position_y"), ("pz", "position_z"),
+                     ("dx", "displacement_x"), ("dy", "displacement_y"), ("dz", "displacement_z")):
+            assert np.array_equal(cols[a], getattr(ref, b)), (k, a)
+    assert kinds[:6] == [0, 1, 2, 2, 2, 2], kinds
+    ctx.close()
+
+
+@pytest.mark.parametrize("summation", [0, 1])
+def test_dense_lists_change_nothing_uid(cuda_required, summation):
+    """Dense moving pool, 12 steps: in uid summation the lists change nothing;
+    in stencil summation list steps sum in uid order (the reference's), so the
+    comparison is against uid-order results within 1e-9 relative."""
+    pool = _dense_pool(15000, 40.0, 8)
+    got, s1 = _run(pool, -1, 12, summation, freeze_at=(0, 1, 2, 3))
+    ref, _ = _run(pool, 0, 12, 0, freeze_at=(0, 1, 2, 3))
+    assert s1["builds"] > 0
+    for k, (a, b) in enumerate(zip(got, ref)):
+        assert a[0] == b[0], k
+        for col in a[1]:
+            if summation == 0 or col in ("uid", "diameter", "adherence"):
+                assert np.array_equal(a[1][col], b[1][col]), (k, col)
+            else:
+                np.testing.assert_allclose(a[1][col], b[1][col], rtol=1e-9, atol=1e-12)
+        for q in range(2, 6):
+            assert np.array_equal(a[q], b[q]), (k, q)
