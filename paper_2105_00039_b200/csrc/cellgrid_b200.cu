@@ -574,11 +574,18 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         if (!c->last_dense) {
             sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
             sweep7_overflow<T, true, false, 16, true><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
-        } else {
-            // dense: z-sorted boxes cut each column run; most agents have more
-            // than 16 partners and take the overflow kernel's rounds
+        } else if (4.19 * (double)A.n / (double)c->geo.nb <= 20.0) {
+            // moderately dense: one thread per agent on z-sorted boxes
             sweep7_kernel<T, true, true, 16, false, 3, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
             sweep7_overflow<T, true, true, 16, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
+        } else {
+            // dense: one warp per agent, the uid-sorted survivor queue is the list;
+            // agents with more than kWarpQ survivors take the overflow kernel's rounds
+            auto k = sweep_warp_kernel<T, true, true>;
+            const size_t sm = sizeof(WarpSmem<T, true>);
+            CUDA_TRY(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k<<<std::min(cdiv(A.n, kThreads / 32), c->sms * 12), kThreads, sm, st>>>(A);
+            sweep7_overflow<T, true, true, 16, true><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
         }
         LAUNCH_CHECK(c);
         c->launches += 2;

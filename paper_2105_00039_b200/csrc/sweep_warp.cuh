@@ -16,6 +16,10 @@
 //     pair forces are stored in that order and lane 0 adds them one by one --
 //     the reference's summation, bit for bit;
 //   * lane 0 runs the epilogue (gate, cap, apply, bbox shell, record).
+// LIST (uid mode only): the list-building sweep of dense pools -- the reach
+// grows by the skin, the walk covers the 5x5 columns (and z +-2) where the
+// reach crosses a box face, and the uid-sorted queue is written out as the
+// agent's neighbour list (partners within r_i + r_j + skin), ballot-compacted.
 #pragma once
 
 #include "common.cuh"
@@ -75,9 +79,49 @@ __device__ __forceinline__ bool pair_force(const Sweep7Args<T> &A, const Rec<T> 
     return true;
 }
 
-template <typename T, bool UIDMODE>
-__global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A)
+// pair_force plus list membership (superset test of dist <= rsum + skin)
+template <typename T>
+__device__ __forceinline__ bool pair_force_l(const Sweep7Args<T> &A, const Rec<T> &me, uint64_t ui, int j,
+                                             T &fx, T &fy, T &fz, int &deg, bool &inl)
 {
+    const T half = T(0.5), zero = A.p.zero;
+    const Rec<T> o = A.rec[j];
+    const T dx = me.x - o.x, dy = me.y - o.y, dz = me.z - o.z;
+    const T ri = me.d * half, rj = o.d * half;
+    const T s2 = dx * dx + dy * dy + dz * dz;
+    const T rsum = ri + rj;
+    const T rs = rsum + A.skin;
+    inl = s2 <= rs * rs * T(1.00001);
+    deg = 0;
+    if (s2 > rsum * rsum * T(1.0000000000009095)) return false;   // fl(sqrt(s2)) > rsum
+    const T dist = tsqrt<T>(s2);
+    const T delta = rsum - dist;
+    if (!(delta > zero)) return false;
+    const T req = (ri * rj) / rsum;
+    const T mag = A.p.kappa * delta - A.p.gamma * tsqrt<T>(req * delta);
+    if (dist > zero) {
+        const T sc = mag / dist;
+        fx = sc * dx;
+        fy = sc * dy;
+        fz = sc * dz;
+    } else {
+        deg = 1;
+        const uint64_t uj = A.uid[j];
+        double ux, uy, uz;
+        degenerate_dir(ui < uj ? ui : uj, ui < uj ? uj : ui, ux, uy, uz);
+        const double sign = ui < uj ? 1.0 : -1.0;
+        fx = (T)((double)mag * (sign * ux));
+        fy = (T)((double)mag * (sign * uy));
+        fz = (T)((double)mag * (sign * uz));
+    }
+    return true;
+}
+
+template <typename T, bool UIDMODE, bool LIST = false>
+__global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Sweep7Args<T> A)
+{
+    static_assert(UIDMODE || !LIST, "lists are built in uid order");
+    constexpr int R = LIST ? 2 : 1, W = 2 * R + 1, NC = W * W;
     extern __shared__ __align__(16) unsigned char wsm[];
     WarpSmem<T, UIDMODE> &S = *reinterpret_cast<WarpSmem<T, UIDMODE> *>(wsm);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -96,9 +140,15 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
         const float mex = __ldg(myp), mey = __ldg(myp + 2), mez = __ldg(myp + 4);
         const Rec<T> me = A.rec[a];
         const uint64_t ui = A.uid[a];
-        const float reach = (float)(me.d * T(0.5)) + A.rmax + A.margin;
+        const float reach = (float)(me.d * T(0.5)) + A.rmax + A.margin + (LIST ? A.skin_f : 0.f);
         const float reach2 = reach * reach;
-        const int z0 = max(iz - 1, 0), z1 = min(iz + 1, A.g.dimz - 1);
+        const int z0m = max(iz - 1, 0), z1m = min(iz + 1, A.g.dimz - 1);
+        int z0 = z0m, z1 = z1m;
+        if (LIST) {   // the boxes two away in z only when the reach crosses the box face
+            const float zl = mez - (float)iz * Lf;
+            if (zl < reach - Lf) z0 = max(iz - 2, 0);
+            if (Lf - zl < reach - Lf) z1 = min(iz + 2, A.g.dimz - 1);
+        }
         int m = -1, qn = 0;
         T fx = zero, fy = zero, fz = zero;   // lane partials (stencil mode)
         int nk = 0, nd = 0;
@@ -122,29 +172,37 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
         // flattened into one candidate index space walked 32 at a time
         int ct0 = 0, clen = 0;
         float cmx = 0.f, cmy = 0.f;
-        if (lane < 9) {
-            const int ox = lane / 3 - 1, oy = lane % 3 - 1;
+        if (lane < NC) {
+            const int ox = lane / W - R, oy = lane % W - R;
             const int nx = ix + ox, ny = iy + oy;
             if ((unsigned)nx < (unsigned)A.g.dimx && (unsigned)ny < (unsigned)A.g.dimy) {
                 const int base = (nx * A.g.dimy + ny) * A.g.dimz;
                 ct0 = __ldg(A.off + base + z0);
                 clen = __ldg(A.off + base + z1 + 1) - ct0;
-                m += clen;   // summed over lanes below
-                const float gx = ox == 0 ? 0.f : fmaxf(0.f, ox < 0 ? mex : Lf - mex);
-                const float gy = oy == 0 ? 0.f : fmaxf(0.f, oy < 0 ? mey : Lf - mey);
+                if (!LIST) {
+                    m += clen;   // summed over lanes below
+                } else if (abs(ox) <= 1 && abs(oy) <= 1) {   // m: the reference's 27 boxes
+                    const int m1 = z1 == z1m ? ct0 + clen : __ldg(A.off + base + z1m + 1);
+                    const int m0 = z0 == z0m ? ct0 : __ldg(A.off + base + z0m);
+                    m += m1 - m0;
+                }
+                const float gx = ox == 0 ? 0.f
+                                         : fmaxf(0.f, (ox < 0 ? mex : Lf - mex) + (float)(abs(ox) - 1) * Lf);
+                const float gy = oy == 0 ? 0.f
+                                         : fmaxf(0.f, (oy < 0 ? mey : Lf - mey) + (float)(abs(oy) - 1) * Lf);
                 if (gx * gx + gy * gy > reach2) clen = 0;
                 cmx = mex - (float)ox * Lf;
                 cmy = mey - (float)oy * Lf;
             }
         }
-        m = (int)__reduce_add_sync(0xffffffffu, (unsigned)(lane < 9 ? m + 1 : 0)) - 1;
-        int cpre = clen;   // inclusive prefix of run lengths over lanes 0-8
+        m = (int)__reduce_add_sync(0xffffffffu, (unsigned)(lane < NC ? m + 1 : 0)) - 1;
+        int cpre = clen;   // inclusive prefix of run lengths over lanes 0..NC-1
 #pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
+        for (int o = 1; o < (LIST ? 32 : 16); o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, cpre, o);
             if (lane >= o) cpre += v;
         }
-        const int total = __shfl_sync(0xffffffffu, cpre, 8);
+        const int total = __shfl_sync(0xffffffffu, cpre, NC - 1);
         const int cex = cpre - clen;   // exclusive prefix
         for (int kb = 0; kb < total; kb += 32) {
             const int k = kb + lane;
@@ -152,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
             // (empty runs share the next run's start, so the last one is non-empty)
             int c = 0;
 #pragma unroll
-            for (int q = 1; q < 9; ++q) c += __shfl_sync(0xffffffffu, cex, q) <= k ? 1 : 0;
+            for (int q = 1; q < NC; ++q) c += __shfl_sync(0xffffffffu, cex, q) <= k ? 1 : 0;
             const int c_t0 = __shfl_sync(0xffffffffu, ct0, c);
             const int c_ex = __shfl_sync(0xffffffffu, cex, c);
             const float mx = __shfl_sync(0xffffffffu, cmx, c), my = __shfl_sync(0xffffffffu, cmy, c);
@@ -227,16 +285,45 @@ __global__ void __launch_bounds__(kThreads, 4) sweep_warp_kernel(Sweep7Args<T> A
                 }
             // pair forces in parallel, summed by lane 0 in uid order
             T(*F)[3] = S.f[wid];
-            for (int p = lane; p < qn; p += 32) {
-                T gx, gy, gz;
-                int dg = 0;
-                const int t = Q[p];
-                const bool kept = pair_force(A, me, ui, storage_of(A, t), gx, gy, gz, dg);
-                F[p][0] = kept ? gx : zero;
-                F[p][1] = kept ? gy : zero;
-                F[p][2] = kept ? gz : zero;
-                nk += kept;
-                nd += dg;
+            if (!LIST) {
+                for (int p = lane; p < qn; p += 32) {
+                    T gx, gy, gz;
+                    int dg = 0;
+                    const int t = Q[p];
+                    const bool kept = pair_force(A, me, ui, storage_of(A, t), gx, gy, gz, dg);
+                    F[p][0] = kept ? gx : zero;
+                    F[p][1] = kept ? gy : zero;
+                    F[p][2] = kept ? gz : zero;
+                    nk += kept;
+                    nd += dg;
+                }
+            } else {
+                // the queue in uid order is the neighbour list (members ballot-compacted)
+                int nl = 0;
+                for (int pb = 0; pb < qn; pb += 32) {
+                    const int p = pb + lane;
+                    bool inl = false;
+                    int j = 0;
+                    if (p < qn) {
+                        T gx = zero, gy = zero, gz = zero;
+                        int dg = 0;
+                        j = storage_of(A, Q[p]);
+                        const bool kept = pair_force_l(A, me, ui, j, gx, gy, gz, dg, inl);
+                        F[p][0] = kept ? gx : zero;
+                        F[p][1] = kept ? gy : zero;
+                        F[p][2] = kept ? gz : zero;
+                        nk += kept;
+                        nd += dg;
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, inl);
+                    const int pos = nl + __popc(bal & lt);
+                    if (inl && pos < A.list_cap) A.nbr[(long long)pos * A.nbr_stride + a] = j;
+                    nl += __popc(bal);
+                }
+                if (lane == 0) {
+                    A.nbr_n[a] = nl;
+                    if (nl > A.list_cap) atomicAdd(A.slots + (blockIdx.x % kSlots) * kSlotWords + 10, 1ull);
+                }
             }
             __syncwarp();
             sx = zero, sy = zero, sz = zero;
