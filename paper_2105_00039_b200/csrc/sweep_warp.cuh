@@ -117,6 +117,59 @@ __device__ __forceinline__ bool pair_force_l(const Sweep7Args<T> &A, const Rec<T
     return true;
 }
 
+// register bitonic sort of the warp's queue Q[0, qn) (qn <= 32 E) by packed
+// (uid32 << 32 | slot) keys, uid32 from the slots' proxies; lane l holds
+// elements [l E, l E + E); Q is rewritten in ascending uid order
+template <int E>
+__device__ __forceinline__ void sort_queue_packed(int *Q, int qn, int lane, const float *prox)
+{
+    constexpr int N = 32 * E;
+    uint64_t a[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        a[e] = ~0ull;
+        if (i < qn) {
+            const int t = Q[i];
+            a[e] = ((uint64_t)__float_as_uint(__ldg(prox + 8 * (t >> 1) + 6 + (t & 1))) << 32) | (unsigned)t;
+        }
+    }
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            if (jj >= E) {   // partner in lane ^ (jj / E), same register
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = lane * E + e;
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, a[e], jj / E);
+                    const bool lower = (i & jj) == 0, up = (i & k) == 0;
+                    a[e] = (lower == up) ? (a[e] < o ? a[e] : o) : (a[e] < o ? o : a[e]);
+                }
+            } else {         // partner in the same lane
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int f = e ^ jj;
+                    if (f > e) {
+                        const bool up = ((lane * E + e) & k) == 0;
+                        const uint64_t x = a[e], y = a[f];
+                        const bool sw = (x > y) == up;
+                        a[e] = sw ? y : x;
+                        a[f] = sw ? x : y;
+                    }
+                }
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        if (i < qn) Q[i] = (int)(unsigned)a[e];
+    }
+    __syncwarp();
+}
+
 template <typename T, bool UIDMODE, bool LIST = false>
 __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Sweep7Args<T> A)
 {
@@ -254,11 +307,27 @@ __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Swee
             // bitonic sort of (uid, slot) by uid over the next power of two
             int np2 = 1;
             while (np2 < qn) np2 <<= 1;
+            // every uid < 2^32: sort packed (uid32 << 32 | slot) keys, uid32 read from
+            // the slot's proxy (no uid gather, no separate slot swaps) -- in
+            // registers up to 256 survivors, else in shared memory
             uint64_t *U = S.u[wid];
+            const bool packed = A.uid32;
+            if (packed && qn <= 64) {
+                sort_queue_packed<2>(Q, qn, lane, A.prox.p);
+                np2 = 0;
+            } else if (packed && qn <= 128) {
+                sort_queue_packed<4>(Q, qn, lane, A.prox.p);
+                np2 = 0;
+            } else if (packed && qn <= 256) {
+                sort_queue_packed<8>(Q, qn, lane, A.prox.p);
+                np2 = 0;
+            }
             for (int p = lane; p < np2; p += 32) {
                 if (p < qn) {
                     const int t = Q[p];
-                    U[p] = A.uid[storage_of(A, t)];
+                    U[p] = packed ? ((uint64_t)__float_as_uint(__ldg(A.prox.p + 8 * (t >> 1) + 6 + (t & 1))) << 32) |
+                                        (unsigned)t
+                                  : A.uid[storage_of(A, t)];
                 } else {
                     U[p] = ~0ull;
                     Q[p] = -1;
@@ -275,14 +344,20 @@ __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Swee
                             if ((u0 > u1) == up) {
                                 U[p] = u1;
                                 U[r] = u0;
-                                const int tq = Q[p];
-                                Q[p] = Q[r];
-                                Q[r] = tq;
+                                if (!packed) {
+                                    const int tq = Q[p];
+                                    Q[p] = Q[r];
+                                    Q[r] = tq;
+                                }
                             }
                         }
                     }
                     __syncwarp();
                 }
+            if (packed && np2) {
+                for (int p = lane; p < qn; p += 32) Q[p] = (int)(unsigned)U[p];
+                __syncwarp();
+            }
             // pair forces in parallel, summed by lane 0 in uid order
             T(*F)[3] = S.f[wid];
             if (!LIST) {
