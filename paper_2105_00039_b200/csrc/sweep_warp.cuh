@@ -261,9 +261,14 @@ __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Swee
             const int k = kb + lane;
             // column of candidate k: the last column whose run starts at or before k
             // (empty runs share the next run's start, so the last one is non-empty)
+            // (binary search over the non-decreasing exclusive prefixes)
             int c = 0;
 #pragma unroll
-            for (int q = 1; q < NC; ++q) c += __shfl_sync(0xffffffffu, cex, q) <= k ? 1 : 0;
+            for (int step = (NC > 16 ? 16 : 8); step > 0; step >>= 1) {
+                const int q = c + step;
+                const int v = __shfl_sync(0xffffffffu, cex, q < NC ? q : NC - 1);
+                if (q < NC && v <= k) c = q;
+            }
             const int c_t0 = __shfl_sync(0xffffffffu, ct0, c);
             const int c_ex = __shfl_sync(0xffffffffu, cex, c);
             const float mx = __shfl_sync(0xffffffffu, cmx, c), my = __shfl_sync(0xffffffffu, cmy, c);
