@@ -105,6 +105,12 @@ struct cg_context {
     unsigned long long *slots = nullptr;
     unsigned long long *maxd_enc = nullptr;
     unsigned *ovf_count = nullptr;
+    // dense uid-mode second pass (sweep_warp BIG): per-warp global queues
+    void *big = nullptr;
+    int big_warps = 0;
+    int *ovf2 = nullptr;
+    unsigned *ovf2_count = nullptr;
+    int64_t ovf2_cap = 0;
     unsigned long long *block_counters = nullptr;   // reference-order sweep only
     double *bbox_dev = nullptr, *bbox_host = nullptr;
     bool bbox_valid = false;
@@ -565,6 +571,50 @@ static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
     return CG_OK;
 }
 
+constexpr int kBigCap = 1024;   // survivors per agent in the second warp pass
+
+// the second pass for dense uid-mode agents that spilled the warp's shared
+// queue (A.ovf), then the thread-per-agent rounds for the few beyond kBigCap
+template <typename T, bool LIST>
+static int launch_sweep_warp_big(cg_context *c, const Sweep7Args<T> &A0)
+{
+    cudaStream_t st = c->stream;
+    const int warps = c->sms * 4 * (kThreads / 32);
+    if (c->big_warps < warps) {
+        if (c->big) cudaFree(c->big);
+        c->big = nullptr;
+        c->big_warps = 0;
+        CUDA_TRY(c, cudaMalloc(&c->big, (size_t)warps * kBigCap * (4 + 8 + 3 * 8)));
+        c->big_warps = warps;
+    }
+    if (!c->ovf2_count) CUDA_TRY(c, cudaMalloc(&c->ovf2_count, sizeof(unsigned)));
+    if (c->ovf2_cap < c->cap) {
+        if (c->ovf2) cudaFree(c->ovf2);
+        c->ovf2 = nullptr;
+        c->ovf2_cap = 0;
+        CUDA_TRY(c, cudaMalloc(&c->ovf2, sizeof(int) * (size_t)std::max<int64_t>(c->cap, 1)));
+        c->ovf2_cap = c->cap;
+    }
+    Sweep7Args<T> A = A0;
+    char *base = (char *)c->big;
+    A.big_cap = kBigCap;
+    A.big_u = (uint64_t *)base;
+    A.big_f = base + (size_t)warps * kBigCap * 8;
+    A.big_q = (int *)(base + (size_t)warps * kBigCap * (8 + 3 * 8));
+    A.ovf2 = c->ovf2;
+    A.ovf2_count = c->ovf2_count;
+    CUDA_TRY(c, cudaMemsetAsync(c->ovf2_count, 0, sizeof(unsigned), st));
+    sweep_warp_kernel<T, true, LIST, true><<<c->sms * 4, kThreads, 0, st>>>(A);
+    LAUNCH_CHECK(c);
+    Sweep7Args<T> B = A;
+    B.ovf = c->ovf2;
+    B.ovf_count = c->ovf2_count;
+    sweep7_overflow<T, true, true, 16, LIST><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(B);
+    LAUNCH_CHECK(c);
+    c->launches += 2;
+    return CG_OK;
+}
+
 template <typename T>
 static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
 {
@@ -580,12 +630,14 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
             sweep7_overflow<T, true, true, 16, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
         } else {
             // dense: one warp per agent, the uid-sorted survivor queue is the list;
-            // agents with more than kWarpQ survivors take the overflow kernel's rounds
+            // agents with more than kWarpQ survivors take the second (global-queue) pass
             auto k = sweep_warp_kernel<T, true, true>;
             const size_t sm = sizeof(WarpSmem<T, true>);
             CUDA_TRY(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             k<<<std::min(cdiv(A.n, kThreads / 32), c->sms * 12), kThreads, sm, st>>>(A);
-            sweep7_overflow<T, true, true, 16, true><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
+            LAUNCH_CHECK(c);
+            c->launches += 1;
+            return launch_sweep_warp_big<T, true>(c, A);
         }
         LAUNCH_CHECK(c);
         c->launches += 2;
@@ -614,9 +666,8 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         CUDA_TRY(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k<<<blocks, kThreads, sm, st>>>(A);
         LAUNCH_CHECK(c);
-        sweep7_overflow<T, true, true, 16><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
-        LAUNCH_CHECK(c);
-        c->launches += 2;
+        c->launches += 1;
+        return launch_sweep_warp_big<T, false>(c, A);
     } else {
         auto k = sweep_warp_kernel<T, false>;
         const size_t sm = sizeof(WarpSmem<T, false>);
@@ -777,7 +828,7 @@ static int list_width_for(const cg_context *c, const Geometry &g, double skin)
     const double r = c->max_diam + skin;
     const double mu = 4.18879 * r * r * r * (double)c->n / vol;
     const int w = ((int)std::ceil(1.25 * mu + 6.0 * std::sqrt(mu) + 16.0) + 15) & ~15;
-    if (w > 512 || (double)w * (double)c->cap * 4.0 > 8e9) return 0;
+    if (w > 1024 || (double)w * (double)c->cap * 4.0 > 16e9) return 0;
     return std::max(w, kListCap);
 }
 
@@ -1703,7 +1754,7 @@ void cg_destroy(cg_context *c)
     for (int *p : ptrs)
         if (p) cudaFree(p);
     void *vptrs[] = {c->scan_status, c->slots, c->maxd_enc, c->ovf_count, c->block_counters, c->bbox_dev, c->stat_dev,
-                     c->maxuid_dev};
+                     c->maxuid_dev, c->big, c->ovf2, c->ovf2_count};
     for (void *p : vptrs)
         if (p) cudaFree(p);
     if (c->bbox_host) cudaFreeHost(c->bbox_host);

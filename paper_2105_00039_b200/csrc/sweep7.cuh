@@ -68,6 +68,14 @@ struct Sweep7Args {
     T skin;
     float skin_f;               // skin rounded up, for the prefilter reach
     int list_cap;               // list entries per agent (more: the list set is not used)
+    // dense uid-mode agents with more survivors than the warp's shared-memory
+    // queue: a second warp pass with per-warp queues in global memory
+    int *big_q;                 // [warps][big_cap]
+    uint64_t *big_u;            // [warps][big_cap]
+    void *big_f;                // [warps][big_cap][3] pool dtype
+    int big_cap;                // power of two
+    int *ovf2;                  // agents beyond big_cap: the thread-per-agent rounds
+    unsigned *ovf2_count;
 };
 
 constexpr int kListCap = 48;    // list width of sparse pools (dense pools: sized from the density)

@@ -170,21 +170,29 @@ __device__ __forceinline__ void sort_queue_packed(int *Q, int qn, int lane, cons
     __syncwarp();
 }
 
-template <typename T, bool UIDMODE, bool LIST = false>
+// BIG: the second pass over the agents the first pass spilled (A.ovf): the
+// same walk, sort and uid-order sum with the warp's queue in global memory
+// (A.big_*, big_cap entries); agents beyond that go to A.ovf2.
+template <typename T, bool UIDMODE, bool LIST = false, bool BIG = false>
 __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Sweep7Args<T> A)
 {
     static_assert(UIDMODE || !LIST, "lists are built in uid order");
+    static_assert(UIDMODE || !BIG, "the global queue is for uid order");
     constexpr int R = LIST ? 2 : 1, W = 2 * R + 1, NC = W * W;
     extern __shared__ __align__(16) unsigned char wsm[];
     WarpSmem<T, UIDMODE> &S = *reinterpret_cast<WarpSmem<T, UIDMODE> *>(wsm);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int *Q = S.q[wid];
+    const int gw = blockIdx.x * (kThreads / 32) + wid;
+    const int QC = BIG ? A.big_cap : kWarpQ;
+    int *Q = BIG ? A.big_q + (size_t)gw * A.big_cap : S.q[wid];
     const unsigned lt = (1u << lane) - 1u;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
     float dmax2 = 0.f;
     const float Lf = (float)A.g.L;
     const T zero = A.p.zero;
-    for (int s = blockIdx.x * (kThreads / 32) + wid; s < A.n; s += gridDim.x * (kThreads / 32)) {
+    const int nunits = BIG ? (int)*A.ovf_count : A.n;
+    for (int w = gw; w < nunits; w += gridDim.x * (kThreads / 32)) {
+        const int s = BIG ? A.ovf[w] : w;
         const int a = storage_of(A, s);
         if ((unsigned)(a - A.own_lo) >= (unsigned)A.n_owned) continue;   // a ghost (uniform across the warp)
         int ix, iy, iz;
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Swee
             const unsigned bal = __ballot_sync(0xffffffffu, pass);
             if (pass) {
                 const int pos = qn + __popc(bal & lt);
-                if (pos < kWarpQ) Q[pos] = t;
+                if (pos < QC) Q[pos] = t;
             }
             qn += __popc(bal);
             if (!UIDMODE && qn > kWarpQ - 32) {
@@ -303,9 +311,12 @@ __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Swee
             snk = __reduce_add_sync(0xffffffffu, (unsigned)nk);
             snd = __reduce_add_sync(0xffffffffu, (unsigned)nd);
         } else {
-            spill = qn > kWarpQ;
-            if (spill) {   // more survivors than the queue holds: the overflow kernel's rounds
-                if (lane == 0) A.ovf[atomicAdd(A.ovf_count, 1u)] = s;
+            spill = qn > QC;
+            if (spill) {   // more survivors than the queue holds: the next pass
+                if (lane == 0) {
+                    if (BIG) A.ovf2[atomicAdd(A.ovf2_count, 1u)] = s;
+                    else A.ovf[atomicAdd(A.ovf_count, 1u)] = s;
+                }
                 __syncwarp();
                 continue;
             }
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Swee
             // every uid < 2^32: sort packed (uid32 << 32 | slot) keys, uid32 read from
             // the slot's proxy (no uid gather, no separate slot swaps) -- in
             // registers up to 256 survivors, else in shared memory
-            uint64_t *U = S.u[wid];
+            uint64_t *U = BIG ? A.big_u + (size_t)gw * A.big_cap : S.u[wid];
             const bool packed = A.uid32;
             if (packed && qn <= 64) {
                 sort_queue_packed<2>(Q, qn, lane, A.prox.p);
@@ -364,7 +375,8 @@ __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Swee
                 __syncwarp();
             }
             // pair forces in parallel, summed by lane 0 in uid order
-            T(*F)[3] = S.f[wid];
+            T(*F)[3] = BIG ? reinterpret_cast<T(*)[3]>(static_cast<T *>(A.big_f) + (size_t)gw * A.big_cap * 3)
+                           : S.f[wid];
             if (!LIST) {
                 for (int p = lane; p < qn; p += 32) {
                     T gx, gy, gz;

@@ -295,3 +295,34 @@ def test_dense_lists_change_nothing_uid(cuda_required, summation):
                 np.testing.assert_allclose(a[1][col], b[1][col], rtol=1e-9, atol=1e-12)
         for q in range(2, 6):
             assert np.array_equal(a[q], b[q]), (k, q)
+
+
+@pytest.mark.parametrize("n,density,skin", [(8000, 350.0, 0), (8000, 350.0, -1), (3000, 1100.0, 0)])
+def test_very_dense_pools_match_oracle(cuda_required, n, density, skin):
+    """More survivors than the warp's shared-memory queue (256): the second
+    warp pass with global queues (<= 1024) and, beyond that, the thread rounds;
+    with lists on, wide lists.  Bit-identical to the oracle in uid order."""
+    from paper_2105_00039_b200 import _native as N
+    from paper_2105_00039_b200.mechanics import ForceParams
+    pool = _dense_pool(n, density, 11)
+    ref = pool.copy()
+    ctx = N.Context(0, pool.dtype)
+    ctx.set_option(N.CG_OPT_SUMMATION, 0)
+    ctx.set_option(N.CG_OPT_LIST_SKIN, skin)
+    ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+    kinds = []
+    for k in range(4):
+        freeze = k < 3
+        st = ctx.step(PARAMS5, None, 1 << 24, N.CG_STEP_SORT | (N.CG_STEP_FREEZE if freeze else 0))
+        kinds.append(int(st.sweep_kind))
+        r = oracle.step(ref, ForceParams(), sort=True, freeze=freeze, threads=8)
+        assert (st.force_evals, st.candidates, st.degenerate_pairs) == (
+            r.force_evals, r.candidates, r.degenerate_pairs), k
+        cols = ctx.download()
+        assert np.array_equal(cols["uid"], ref.uid)
+        for a, b in (("px", "position_x"), ("py", "position_y"), ("pz", "position_z"),
+                     ("dx", "displacement_x"), ("dy", "displacement_y"), ("dz", "displacement_z")):
+            assert np.array_equal(cols[a], getattr(ref, b)), (k, a)
+    if skin:
+        assert kinds[:3] == [0, 1, 2], kinds
+    ctx.close()
