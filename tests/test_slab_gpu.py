@@ -15,9 +15,13 @@ pytestmark = pytest.mark.gpu
 PARAMS5 = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
 
 
-def _pool(fp32=False):
+def _pool(fp32=False, dense=False):
     from paper_2105_00039_b200.pool import AgentPool, PrecisionMode
     from paper_2105_00039_b200.workloads import jittered_lattice_positions
+    if dense:   # ~350 partners per agent: the warp sweep's second (global-queue) pass
+        from paper_2105_00039_b200.geometry import Aabb
+        from paper_2105_00039_b200.workloads import box_side_for_density
+        return AgentPool.spawn_random(6000, Aabb.cube(box_side_for_density(6000, 10.0, 350.0)), 10.0, 0.4, 4)
     pos = jittered_lattice_positions(20, spacing=7.0, jitter=1.0, seed=5)
     pos[:, 0] *= 1.4
     return AgentPool.from_arrays(pos, 10.0, 0.4, PrecisionMode.FP32 if fp32 else PrecisionMode.FP64)
@@ -31,7 +35,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1, fp32=False):
+def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1, fp32=False, dense=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -41,7 +45,7 @@ def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1, fp32=F
     from paper_2105_00039_b200.distributed import SlabRunner, TorchExchange
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % port, rank=rank, world_size=world)
-    full = _pool(fp32)
+    full = _pool(fp32, dense)
     mine = (full.uid % world) == rank            # ignores the slab rule: step 1 migrates
     ctx = _native.Context(0, full.dtype)
     ctx.set_option(_native.CG_OPT_SUMMATION, summation)
@@ -63,7 +67,8 @@ def _worker(rank, world, port, steps, params5, summation, out_q, skin=-1, fp32=F
     (2, 0, 0, (2.0, 1.0, 0.01, 3.0, 1.0)), (3, 1, 0, (2.0, 1.0, 0.01, 3.0, 1.0)),
     (2, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)), (3, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)),
     (5, 0, -1, (2.0, 1.0, 0.002, 3.0, 1.0)),    # 5 slabs of ~4 planes: ghost bands reach two ranks away
-    (3, 0, -2, (2.0, 1.0, 0.002, 3.0, 1.0))])   # skin -2: lists on, fp32 pool
+    (3, 0, -2, (2.0, 1.0, 0.002, 3.0, 1.0)),    # skin -2: lists on, fp32 pool
+    (2, 0, -3, (2.0, 1.0, 0.01, 3.0, 1.0))])    # skin -3: dense pool (no slab lists), uid order
 def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, params):
     """skin 0: a full exchange every step; skin -1: neighbour lists, the
     partition frozen and the ghosts refreshed between rebuilds (small
@@ -71,13 +76,14 @@ def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, 
     import multiprocessing as mp
     from paper_2105_00039_b200 import _native
     PARAMS5 = np.array(params)
-    steps = 4 if skin == 0 else 9
+    dense = skin == -3
+    steps = 4 if skin in (0, -3) else 9
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
     port = _free_port()
     fp32 = skin == -2
-    skin = -1 if fp32 else skin
-    procs = [mpc.Process(target=_worker, args=(r, world, port, steps, PARAMS5, summation, q, skin, fp32))
+    skin = -1 if fp32 else (0 if dense else skin)
+    procs = [mpc.Process(target=_worker, args=(r, world, port, steps, PARAMS5, summation, q, skin, fp32, dense))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -86,7 +92,7 @@ def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, 
         p.join(timeout=120)
         assert p.exitcode == 0
     # single-context run of the global pool
-    full = _pool(fp32)
+    full = _pool(fp32, dense)
     ctx = _native.Context(0, full.dtype)
     ctx.set_option(_native.CG_OPT_SUMMATION, summation)
     ctx.upload(full.position_x, full.position_y, full.position_z, full.diameter, full.adherence, full.uid)
