@@ -1072,9 +1072,9 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
             build = c->list_skin_used > 0 && c->list_skin_used <= g.L;
             c->list_width = build ? list_width_for(c, g, c->list_skin_used) : 0;
             build = build && c->list_width > 0;
-            // dense pools: no build while the last moving grid sweep moved some
-            // agent by more than skin / 4 (the lists would not serve 2 steps)
-            if (build && c->list_width != kListCap && !freeze && c->last_kind == 0 && !c->last_freeze &&
+            // dense pools: no build while the last moving step moved some agent by
+            // more than skin / 4 (the lists would not serve 2 steps)
+            if (build && c->list_width != kListCap && !freeze && !c->last_freeze &&
                 4.0 * std::sqrt(std::max(c->bbox_host[7], 0.0)) > c->list_skin_used)
                 build = false;
             if (build && (rc = ensure_lists(c, c->list_width))) return rc;
