@@ -28,6 +28,9 @@
 
 namespace cg {
 
+#ifndef CG_WARP_REG_SORT
+#define CG_WARP_REG_SORT 1   // 0: every uid sort in shared memory (A/B switch)
+#endif
 constexpr int kWarpQ = 256;   // survivors queued per warp before a flush (stencil mode)
 
 template <typename T, bool UIDMODE>
@@ -328,7 +331,8 @@ __global__ void __launch_bounds__(kThreads, LIST ? 3 : 4) sweep_warp_kernel(Swee
             // registers up to 256 survivors, else in shared memory
             uint64_t *U = BIG ? A.big_u + (size_t)gw * A.big_cap : S.u[wid];
             const bool packed = A.uid32;
-            if (packed && qn <= 64) {
+            if (!CG_WARP_REG_SORT) {
+            } else if (packed && qn <= 64) {
                 sort_queue_packed<2>(Q, qn, lane, A.prox.p);
                 np2 = 0;
             } else if (packed && qn <= 128) {
