@@ -460,6 +460,9 @@ static int materialize_presentation(cg_context *c, cudaStream_t st = nullptr)
 
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
 // idx (or, when relayout, the records in slot order in the alternate buffers).
+static int ensure_big(cg_context *c);
+static int ensure_lists(cg_context *c, int width);
+static int list_width_for(const cg_context *c, const Geometry &g, double skin);
 template <typename T>
 static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort, int rot = 0);
 
@@ -542,6 +545,12 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
         c->launches += 1;
     }
     c->last_dense = dense;
+    if (dense && (rc = ensure_big(c))) return rc;   // the warp sweep's second-pass queues
+    if (dense && c->list_skin != 0.0 && c->sweep_impl == 1 && c->n > 1) {
+        // the lists a later build will need, allocated now (outside the build step)
+        const int w = list_width_for(c, g, c->list_skin < 0 ? 0.07 * g.L : c->list_skin);
+        if (w > 0 && (rc = ensure_lists(c, w))) return rc;
+    }
     if (relayout) {
         c->cur_pos = o;
         c->cur_attr = oa;
@@ -575,10 +584,8 @@ constexpr int kBigCap = 1024;   // survivors per agent in the second warp pass
 
 // the second pass for dense uid-mode agents that spilled the warp's shared
 // queue (A.ovf), then the thread-per-agent rounds for the few beyond kBigCap
-template <typename T, bool LIST>
-static int launch_sweep_warp_big(cg_context *c, const Sweep7Args<T> &A0)
+static int ensure_big(cg_context *c)
 {
-    cudaStream_t st = c->stream;
     const int warps = c->sms * 4 * (kThreads / 32);
     if (c->big_warps < warps) {
         if (c->big) cudaFree(c->big);
@@ -595,6 +602,16 @@ static int launch_sweep_warp_big(cg_context *c, const Sweep7Args<T> &A0)
         CUDA_TRY(c, cudaMalloc(&c->ovf2, sizeof(int) * (size_t)std::max<int64_t>(c->cap, 1)));
         c->ovf2_cap = c->cap;
     }
+    return CG_OK;
+}
+
+template <typename T, bool LIST>
+static int launch_sweep_warp_big(cg_context *c, const Sweep7Args<T> &A0)
+{
+    cudaStream_t st = c->stream;
+    int rc = ensure_big(c);   // normally done when the grid turned dense
+    if (rc) return rc;
+    const int warps = c->big_warps;
     Sweep7Args<T> A = A0;
     char *base = (char *)c->big;
     A.big_cap = kBigCap;
@@ -798,7 +815,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
 }
 
 // ---------------------------------------------------------------- neighbour-list reuse
-static int ensure_lists(cg_context *c, int width = kListCap)
+static int ensure_lists(cg_context *c, int width)
 {
     if (c->nbr && c->nbr_cap == c->cap && c->nbr_width >= width) return CG_OK;
     if (c->nbr) cudaFree(c->nbr);
@@ -1638,7 +1655,7 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
             build = S.B.band == 3 && c->list_wait == 0 && !c->last_dense;
             if (c->list_wait > 0) c->list_wait--;
             if (build) {
-                if ((rc = ensure_lists(c))) return rc;
+                if ((rc = ensure_lists(c, kListCap))) return rc;
                 c->list_width = kListCap;
                 c->list_skin_used = c->list_skin < 0 ? 0.07 * S.g.L : c->list_skin;
                 build = c->list_skin_used > 0 && c->list_skin_used <= S.g.L;
