@@ -28,6 +28,9 @@
 
 namespace cg {
 
+#ifndef CG_WARP_MINB
+#define CG_WARP_MINB 4       // stencil-mode blocks per SM (uid mode: 3, shared-memory bound)
+#endif
 #ifndef CG_WARP_REG_SORT
 #define CG_WARP_REG_SORT 1   // 0: every uid sort in shared memory (A/B switch)
 #endif
@@ -177,7 +180,7 @@ __device__ __forceinline__ void sort_queue_packed(int *Q, int qn, int lane, cons
 // same walk, sort and uid-order sum with the warp's queue in global memory
 // (A.big_*, big_cap entries); agents beyond that go to A.ovf2.
 template <typename T, bool UIDMODE, bool LIST = false, bool BIG = false>
-__global__ void __launch_bounds__(kThreads, UIDMODE ? 3 : 4) sweep_warp_kernel(Sweep7Args<T> A)   // uid mode: 3 blocks by shared memory anyway
+__global__ void __launch_bounds__(kThreads, UIDMODE ? 3 : CG_WARP_MINB) sweep_warp_kernel(Sweep7Args<T> A)   // uid mode: 3 blocks by shared memory anyway
 {
     static_assert(UIDMODE || !LIST, "lists are built in uid order");
     static_assert(UIDMODE || !BIG, "the global queue is for uid order");
