@@ -36,6 +36,9 @@
 
 #include "../../include/cellgrid_b200.h"
 
+#ifndef CG_KEY32
+#define CG_KEY32 1   // sparse sweeps: 32-bit uid sort keys when every uid < 2^32 (0: 64-bit)
+#endif
 #ifndef CG_LIST_BUILD_MINB
 #define CG_LIST_BUILD_MINB 4   // the same sweep building neighbour lists
 #endif
@@ -564,16 +567,16 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
     return CG_OK;
 }
 
-template <typename T, bool UID, bool ZS, int KS, bool FLUSH, int MINB>
+template <typename T, bool UID, bool ZS, int KS, bool FLUSH, int MINB, bool KEY32 = false>
 static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
 {
     cudaStream_t st = c->stream;
     CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
-    sweep7_kernel<T, UID, ZS, KS, FLUSH, MINB><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
+    sweep7_kernel<T, UID, ZS, KS, FLUSH, MINB, false, KEY32><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
     LAUNCH_CHECK(c);
     c->launches += 1;
     if (!FLUSH) {   // agents with more than KS survivors (none in most steps)
-        sweep7_overflow<T, UID, ZS, KS><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
+        sweep7_overflow<T, UID, ZS, KS, false, KEY32><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
         LAUNCH_CHECK(c);
         c->launches += 1;
     }
@@ -639,8 +642,14 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         cudaStream_t st = c->stream;
         CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
         if (!c->last_dense) {
-            sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
-            sweep7_overflow<T, true, false, 16, true><<<std::min(cdiv(A.n, kThreads), c->sms * 2), kThreads, 0, st>>>(A);
+            const int g1 = cdiv(A.n, kThreads), g2 = std::min(cdiv(A.n, kThreads), c->sms * 2);
+            if (CG_KEY32 && A.uid32) {
+                sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true, true><<<g1, kThreads, 0, st>>>(A);
+                sweep7_overflow<T, true, false, 16, true, true><<<g2, kThreads, 0, st>>>(A);
+            } else {
+                sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true><<<g1, kThreads, 0, st>>>(A);
+                sweep7_overflow<T, true, false, 16, true><<<g2, kThreads, 0, st>>>(A);
+            }
         } else if (4.19 * (double)A.n / (double)c->geo.nb <= 20.0) {
             // moderately dense: one thread per agent on z-sorted boxes
             sweep7_kernel<T, true, true, 16, false, 3, true><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
@@ -664,6 +673,7 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         // sparse: survivors summed in uid order (deterministic and bit-identical to
         // the reference whatever the slot order in a box); agents with more than
         // 16 survivors go to the overflow kernel
+        if (CG_KEY32 && A.uid32) return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB, true>(c, A);
         return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB>(c, A);
     }
     // moderately dense (<= 20 expected survivors): one thread per agent

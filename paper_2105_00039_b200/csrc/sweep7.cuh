@@ -29,6 +29,8 @@
 // exactly what _gather_stencil enumerates.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "grid.cuh"
 #include "sweep.cuh"
@@ -127,12 +129,14 @@ __device__ __forceinline__ void f2_unpack(f32x2 v, float &lo, float &hi)
 // agent's neighbour list; the walk then covers the 5x5x5 box stencil (a
 // partner within ri + rmax + skin <= 2L can sit two boxes away), while m still
 // counts the reference's 27 boxes.
-template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, bool DEFER, bool LIST = false>
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, bool DEFER, bool LIST = false,
+          bool KEY32 = false>
 __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s, unsigned &c_m,
                                             unsigned &c_nk, unsigned &c_nd, float &dmax2)
 {
     __shared__ int lst[KS][kThreads];
-    __shared__ uint64_t ukey[UIDMODE ? KS : 1][kThreads];
+    // KEY32: every uid < 2^32 (A.uid32): 32-bit sort keys from the proxies
+    __shared__ typename std::conditional<KEY32, uint32_t, uint64_t>::type ukey[UIDMODE ? KS : 1][kThreads];
     static_assert(!(UIDMODE && FLUSH), "uid order needs the whole list");
 #define LST(k) lst[k][threadIdx.x]
 #define UKEY(k) ukey[k][threadIdx.x]
@@ -347,7 +351,8 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 [&](int t, unsigned u) {
                     if (ns < KS) {
                         LST(ns) = t;
-                        UKEY(ns) = A.uid32 ? (uint64_t)u : cand_uid(t);
+                        if (KEY32) UKEY(ns) = u;
+                        else UKEY(ns) = A.uid32 ? (uint64_t)u : cand_uid(t);
                         ++ns;
                     }
                     ++total;
@@ -381,7 +386,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                     int nr = 0;
                     walk(
                         [&](int t, unsigned u) {
-                            const uint64_t ut = A.uid32 ? (uint64_t)u : cand_uid(t);
+                            const uint64_t ut = (KEY32 || A.uid32) ? (uint64_t)u : cand_uid(t);
                             if (!first && ut <= floor_uid) return;
                             int q;
                             if (nr < KS) q = nr++;
@@ -478,27 +483,27 @@ __device__ __forceinline__ void warp_dmax(unsigned long long *slots, float dmax2
         atomicMax(slots + (blockIdx.x % kSlots) * kSlotWords + 9, enc_ordered((double)dmax2));
 }
 
-template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, int MINB, bool LIST = false>
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, int MINB, bool LIST = false, bool KEY32 = false>
 __global__ void __launch_bounds__(kThreads, MINB) sweep7_kernel(Sweep7Args<T> A)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
     float dmax2 = 0.f;
-    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true, LIST>(A, s, c_m, c_nk, c_nd, dmax2);
+    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true, LIST, KEY32>(A, s, c_m, c_nk, c_nd, dmax2);
     warp_counters(A.slots, c_m, c_nk, c_nd);
     if (LIST || ZSORTED) warp_dmax(A.slots, dmax2);
 }
 
 // agents deferred by sweep7_kernel (more than KS survivors): grid-stride over
 // the device-side list, further walks per agent
-template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool LIST = false>
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool LIST = false, bool KEY32 = false>
 __global__ void __launch_bounds__(kThreads) sweep7_overflow(Sweep7Args<T> A)
 {
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
     float dmax2 = 0.f;
     const unsigned cnt = *A.ovf_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
-        sweep_agent<T, UIDMODE, ZSORTED, KS, false, false, LIST>(A, A.ovf[k], c_m, c_nk, c_nd, dmax2);
+        sweep_agent<T, UIDMODE, ZSORTED, KS, false, false, LIST, KEY32>(A, A.ovf[k], c_m, c_nk, c_nd, dmax2);
     warp_counters(A.slots, c_m, c_nk, c_nd);
     if (LIST || ZSORTED) warp_dmax(A.slots, dmax2);
 }
