@@ -47,17 +47,54 @@ struct ListArgs {
     double shell_lo[3], shell_hi[3];
 };
 
-// coincident centres (kernels.py:244-257): out of line, it is rare and its
-// transcendental code would otherwise hold registers in the pair loop
 template <typename T>
-__device__ __noinline__ void degenerate_pair(uint64_t ui, uint64_t uj, T mag, T &fx, T &fy, T &fz)
+struct AgentSum {
+    T fx, fy, fz;
+    int nk, nd;
+};
+
+// The whole pair sum of one agent with the library's sqrt and division and
+// the coincident-centre branch (kernels.py:244-257).  The pair loops run a
+// call-free fast path (common.cuh) and hand an agent here when an operand
+// leaves its range or two centres coincide -- rare, so out of line.
+template <typename T>
+__device__ __noinline__ AgentSum<T> list_agent_slow(const Rec<T> *__restrict__ rec, const uint64_t *__restrict__ uid,
+                                                     const int *__restrict__ L, long long stride, int cnt, int a,
+                                                     T kappa, T gamma, T zero)
 {
-    double ux, uy, uz;
-    degenerate_dir(ui < uj ? ui : uj, ui < uj ? uj : ui, ux, uy, uz);
-    const double sign = ui < uj ? 1.0 : -1.0;
-    fx = fx + (T)((double)mag * (sign * ux));
-    fy = fy + (T)((double)mag * (sign * uy));
-    fz = fz + (T)((double)mag * (sign * uz));
+    const T half = T(0.5);
+    const Rec<T> me = rec[a];
+    const T ri = me.d * half;
+    AgentSum<T> S{zero, zero, zero, 0, 0};
+    for (int p = 0; p < cnt; ++p) {
+        const int j = L[p * stride];
+        const Rec<T> co = rec[j];
+        const T dx = me.x - co.x, dy = me.y - co.y, dz = me.z - co.z;
+        const T rj = co.d * half;
+        const T dist = tsqrt<T>(dx * dx + dy * dy + dz * dz);
+        const T rsum = ri + rj;
+        const T delta = rsum - dist;
+        if (!(delta > zero)) continue;
+        ++S.nk;
+        const T req = (ri * rj) / rsum;
+        const T mag = kappa * delta - gamma * tsqrt<T>(req * delta);
+        if (dist > zero) {
+            const T sc = mag / dist;
+            S.fx = S.fx + sc * dx;
+            S.fy = S.fy + sc * dy;
+            S.fz = S.fz + sc * dz;
+        } else {
+            const uint64_t ui = uid[a], uj = uid[j];
+            double ux, uy, uz;
+            degenerate_dir(ui < uj ? ui : uj, ui < uj ? uj : ui, ux, uy, uz);
+            const double sign = ui < uj ? 1.0 : -1.0;
+            S.fx = S.fx + (T)((double)mag * (sign * ux));
+            S.fy = S.fy + (T)((double)mag * (sign * uy));
+            S.fz = S.fz + (T)((double)mag * (sign * uz));
+            ++S.nd;
+        }
+    }
+    return S;
 }
 
 #ifndef CG_LIST_THREADS
@@ -68,24 +105,39 @@ constexpr int kListThreads = CG_LIST_THREADS;
 #define CG_LIST_MINB 4
 #endif
 
+// s2 > rsum^2 (1 + 2^-40) implies fl(sqrt(s2)) > rsum, i.e. delta <= 0: the
+// pair cannot be kept and needs no sqrt.  The factor is representable in both
+// dtypes only for fp64; fp32 uses 1 + 4 eps (both rely on a correctly rounded
+// sqrt, the library's -prec-sqrt=true default).
+template <typename T>
+__device__ __forceinline__ T reject_factor();
+template <>
+__device__ __forceinline__ double reject_factor<double>() { return 1.0000000000009095; }
+template <>
+__device__ __forceinline__ float reject_factor<float>() { return 1.00000048f; }
+
 // FUSED: the step's box counting is done here (box id of the current
 // position, one atomic per run of equal keys in the warp) instead of in a
 // separate box_keys pass; m and the grid statistics then come from the
 // per-box pass box_stencil_pass (a step without CG_STEP_RECORD).
+//
+// The pair loop is call-free (sqrt_nocall / div_nocall, common.cuh): an agent
+// whose operands leave the fast range, or with coincident centres, is redone
+// by list_agent_slow.  Entries are consumed in list (uid) order, so the sums
+// are the reference's.
 template <typename T, bool FUSED = false>
 __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(ListArgs<T> A)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int a = A.own_lo + t;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
     float dmax2 = 0.f;
-    if (FUSED) {
+    if (FUSED) {   // storage order: runs of equal box keys within the warp
         const int lane = threadIdx.x & 31;
         int flat = -1 - lane;   // distinct dummy keys past n
         if (t < A.n) {
-            const Rec<T> r = A.rec[a];
+            const Rec<T> r = A.rec[A.own_lo + t];
             flat = flat_box_fast(A.g, A.invL, r.x, r.y, r.z);
-            if (A.pkey) A.pkey[a] = flat;
+            if (A.pkey) A.pkey[A.own_lo + t] = flat;
         }
         const int prev = __shfl_up_sync(0xffffffffu, flat, 1);
         const bool start = lane == 0 || prev != flat;
@@ -95,6 +147,7 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
         if (start && t < A.n) atomicAdd(A.count + flat, run_end - lane);
     }
     if (t < A.n) {
+        const int a = A.own_lo + t;
         int m = -1;
         if (!FUSED) {
         const int key = A.key_rank[a].x;
@@ -122,48 +175,51 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
         const Rec<T> me = A.rec[a];
         const T xi = me.x, yi = me.y, zi = me.z;
         const T ri = me.d * half;
+        const T kfac = reject_factor<T>();
         T fx = zero, fy = zero, fz = zero;
         int nk = 0, nd = 0;
+        bool ok = true;
         T last_rj = T(-1), last_req = zero;
         const int cnt = A.nbr_n[a];
         const int *L = A.nbr + a;
-        // two indices and one record ahead of the pair being evaluated
+        // two indices and one record ahead of the entry being tested
         int jn = cnt > 0 ? __ldg(L) : 0;
         int jnn = cnt > 1 ? __ldg(L + A.nbr_stride) : 0;
         Rec<T> o;
         if (cnt > 0) o = A.rec[jn];
 #pragma unroll 1
         for (int p = 0; p < cnt; ++p) {
-            const int jc = jn;
             const Rec<T> co = o;
             jn = jnn;
             if (p + 1 < cnt) o = A.rec[jn];
             if (p + 2 < cnt) jnn = __ldg(L + (p + 2) * A.nbr_stride);
-            // the reference's pass-1 test and pass-2 expressions (kernels.py:198-257)
             const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;
             const T rj = co.d * half;
             const T s2 = dx * dx + dy * dy + dz * dz;
             const T rsum = ri + rj;
-            // s2 > rsum^2 (1 + 2^-40) implies fl(sqrt(s2)) > rsum: not overlapping, no sqrt needed
-            if (s2 > rsum * rsum * T(1.0000000000009095)) continue;
-            const T dist = tsqrt<T>(s2);
+            if (s2 > rsum * rsum * kfac) continue;
+            const T dist = tsqrt_nocall(s2, ok);
             const T delta = rsum - dist;
             if (!(delta > zero)) continue;
             ++nk;
             if (rj != last_rj) {
                 last_rj = rj;
-                last_req = (ri * rj) / rsum;
+                last_req = tdiv_nocall(ri * rj, rsum, ok);
             }
-            const T mag = A.p.kappa * delta - A.p.gamma * tsqrt<T>(last_req * delta);
-            if (dist > zero) {
-                const T sc = mag / dist;
-                fx = fx + sc * dx;
-                fy = fy + sc * dy;
-                fz = fz + sc * dz;
-            } else {
-                degenerate_pair(A.uid[a], A.uid[jc], mag, fx, fy, fz);
-                ++nd;
-            }
+            const T mag = A.p.kappa * delta - A.p.gamma * tsqrt_nocall(last_req * delta, ok);
+            const T sc = tdiv_nocall(mag, dist, ok);   // dist == 0 (coincident centres): not ok
+            fx = fx + sc * dx;
+            fy = fy + sc * dy;
+            fz = fz + sc * dz;
+            if (!ok) break;
+        }
+        if (!ok) {
+            const AgentSum<T> S = list_agent_slow<T>(A.rec, A.uid, L, A.nbr_stride, cnt, a, A.p.kappa, A.p.gamma, zero);
+            fx = S.fx;
+            fy = S.fy;
+            fz = S.fz;
+            nk = S.nk;
+            nd = S.nd;
         }
         // _write_displacement, kernels.py:266-277
         const T norm = tsqrt<T>(fx * fx + fy * fy + fz * fz);

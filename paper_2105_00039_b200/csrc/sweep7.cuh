@@ -253,6 +253,14 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         T fx = zero, fy = zero, fz = zero;
         int nk = 0, nd = 0, nl = 0;
         T last_rj = T(-1), last_req = zero;
+        // NOCALL (the main kernel when an overflow kernel follows): call-free
+        // sqrt / division (common.cuh); an operand outside their fast range,
+        // or coincident centres, hands the agent to the overflow kernel,
+        // which uses the library routines
+        constexpr bool NOCALL = DEFER && !FLUSH;
+        bool ok = true;
+        auto xsqrt = [&](T v) -> T { return NOCALL ? tsqrt_nocall(v, ok) : tsqrt<T>(v); };
+        auto xdiv = [&](T a_, T b_) -> T { return NOCALL ? tdiv_nocall(a_, b_, ok) : a_ / b_; };
         // phase 2 for list entries [0, cnt), in list order; the next entry's
         // record is in flight while the current pair is evaluated
         auto evaluate = [&](int cnt_) {
@@ -273,7 +281,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 }
                 const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;   // kernels.py:198-203
                 const T rj = co.d * half;
-                const T dist = tsqrt<T>(dx * dx + dy * dy + dz * dz);
+                const T dist = xsqrt(dx * dx + dy * dy + dz * dz);
                 const T rsum = ri + rj;
                 if (LIST && dist <= rsum + A.skin) {
                     if (nl < A.list_cap) A.nbr[nl * A.nbr_stride + a] = jc;
@@ -284,11 +292,11 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 ++nk;                                                    // kernels.py:230-257
                 if (rj != last_rj) {
                     last_rj = rj;
-                    last_req = (ri * rj) / rsum;
+                    last_req = xdiv(ri * rj, rsum);
                 }
-                const T mag = A.p.kappa * delta - A.p.gamma * tsqrt<T>(last_req * delta);
-                if (dist > zero) {
-                    const T sc = mag / dist;
+                const T mag = A.p.kappa * delta - A.p.gamma * xsqrt(last_req * delta);
+                if (NOCALL || dist > zero) {   // NOCALL: dist == 0 fails the division's range test
+                    const T sc = xdiv(mag, dist);
                     fx = fx + sc * dx;
                     fy = fy + sc * dy;
                     fz = fz + sc * dz;
@@ -409,6 +417,10 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             }
         }
 
+        if (NOCALL && !ok) {   // redone by the overflow kernel (library sqrt / division)
+            A.ovf[atomicAdd(A.ovf_count, 1u)] = s;
+            return;
+        }
         // _write_displacement, kernels.py:266-277
         const T norm = tsqrt<T>(fx * fx + fy * fy + fz * fz);
         T ddx = zero, ddy = zero, ddz = zero;
