@@ -48,7 +48,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", help="c4 (default), c2, c1, c3_<density>")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
-    ap.add_argument("--summation", default="stencil", choices=["uid", "stencil"])
+    ap.add_argument("--summation", default="uid", choices=["uid", "stencil"],
+                    help="dense pools only (sparse pools always sum each agent's pairs in uid order, "
+                         "the reference's order)")
     ap.add_argument("--relayout-every", type=int, default=1,
                     help="move records into slot order on every k-th sort step")
     ap.add_argument("--sort-every", type=int, default=1)
@@ -63,16 +65,42 @@ def parse():
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (testing)")
     ap.add_argument("--force-slab", action="store_true",
                     help="run the slab (multi-GPU) driver even at world size 1 (exercises the exchange)")
+    ap.add_argument("--side", type=int, default=256,
+                    help="lattice side of C4 (and of each rank's C5 slab): 256 = the BASELINE config")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the other BASELINE configs (C4 lists off, C2, C3 sweep) in the N=1 line")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="start the N ranks, initialise the process group, print world and exit (no GPU work)")
     return ap.parse_args()
 
 
-def make_pool(name, precision, rank=0, world=1):
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_relaunch(args):
+    """``bench.py --gpus N`` (N > 1) outside torchrun: re-run this command as N
+    ranks under torch.distributed.run on 127.0.0.1, one process per GPU."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")     # the communicator lines show N ranks
+    env.setdefault("OMP_NUM_THREADS", "1")
+    raise SystemExit(subprocess.call(cmd, env=env))
+
+
+def make_pool(name, precision, rank=0, world=1, side=256):
     from paper_2105_00039_b200 import workloads
     from paper_2105_00039_b200.pool import PrecisionMode
     pm = PrecisionMode.FP64 if precision == "fp64" else PrecisionMode.FP32
     if name == "c4":
-        return (workloads.c4(pm) if world == 1 else workloads.c5_shard(rank, world, pm)), \
-            "C4: 256^3 jittered lattice (spacing 8, diameter 10, jitter +-1), 16,777,216 agents" + \
+        return (workloads.c4(pm, side) if world == 1 else workloads.c5_shard(rank, world, pm, side)), \
+            "C4: %d^3 jittered lattice (spacing 8, diameter 10, jitter +-1), %s agents" % (side, format(side ** 3, ",")) + \
             ("" if world == 1 else " per rank (C5 slab %d of %d)" % (rank, world))
     if name == "c2":
         return workloads.c2(pm), "C2: 1M uniform random, ref-density 27"
@@ -204,18 +232,24 @@ def dist_init(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.same_device:
         local = 0
+    if world != args.gpus and rank == 0:
+        print("bench.py: --gpus %d but WORLD_SIZE=%d; running %d rank(s)" % (args.gpus, world, world),
+              file=sys.stderr)
     if world > 1 or (args.force_slab and args.impl == "ours"):
         import torch
         import torch.distributed as dist
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("MASTER_PORT", str(free_port()))
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        torch.cuda.set_device(local)
         if args.exchange == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
+            if torch.cuda.is_available() and not args.launch_check:
+                torch.cuda.set_device(local)
             dist.init_process_group("gloo")
     return rank, world, local
 
@@ -240,7 +274,7 @@ def barrier(world):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    pool, desc = make_pool(args.config, args.precision)
+    pool, desc = make_pool(args.config, args.precision, side=args.side)
     n = pool.count
     # bounded sample: the full workload while K+W full steps fit in ~3 min, else fewer steps
     t_one, th = cpu_port_run(pool, args.precision, 1, args.sort_every, args.freeze)
@@ -253,7 +287,7 @@ def run_reference(args, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": {"workload": desc, "agents": n, "sort_every": args.sort_every,
                        "freeze": args.freeze, "cpu_threads": th},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": "port",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": "port", "cpu_model": cpu_model(),
                              "sample": "%d full step(s) of the %d-agent workload (requested K+W=%d)"
                                        % (k_run, n, k_total)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -269,7 +303,7 @@ def main_slab(args, rank, world, local):
     from paper_2105_00039_b200 import _native
     from paper_2105_00039_b200.distributed import SlabRunner, TorchExchange
     torch.cuda.set_device(local)
-    pool, desc = make_pool(args.config, args.precision, rank, world)
+    pool, desc = make_pool(args.config, args.precision, rank, world, args.side)
     n0 = pool.count
     ctx = _native.Context(local, pool.dtype)
     ctx.set_option(_native.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[args.summation])
@@ -353,8 +387,8 @@ def main_slab(args, rank, world, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-        "config": {"workload": "C5: (256 x %d) x 256 x 256 jittered lattice, %d agents (%d per GPU at start)"
-                               % (world, total, n0),
+        "config": {"workload": "C5: (%d x %d) x %d x %d jittered lattice, %d agents (%d per GPU at start)"
+                               % (args.side, world, args.side, args.side, total, n0),
                    "agents_total": total, "summation": args.summation, "freeze": args.freeze,
                    "l2": "inputs larger than L2 (%.0f MB of agent state per GPU)" % (n0 * 64 / 1e6),
                    "parallelism": "x-slabs x%d over %s: migration + ghost exchange on rebuild steps, ghost refresh on "
@@ -374,9 +408,103 @@ def main_slab(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+EXTRAS = (   # (key, config, precision, summation, list skin, sort_every, freeze) -- BASELINE.json configs
+    ("c4_lists_off", "c4", "fp64", "uid", 0, 1, False),     # the literal "grid rebuild each step"
+    ("c2_fp64", "c2", "fp64", "uid", -1, 1, False),
+    ("c2_fp32", "c2", "fp32", "uid", -1, 1, False),
+    ("c2_fp64_stencil_sum", "c2", "fp64", "stencil", -1, 1, False),
+    ("c3_4_sorted", "c3_4", "fp64", "uid", -1, 1, True),
+    ("c3_4_unsorted", "c3_4", "fp64", "uid", -1, 0, True),
+    ("c3_27_sorted", "c3_27", "fp64", "uid", -1, 1, True),
+    ("c3_27_unsorted", "c3_27", "fp64", "uid", -1, 0, True),
+    ("c3_100_sorted", "c3_100", "fp64", "uid", -1, 1, True),
+    ("c3_100_unsorted", "c3_100", "fp64", "uid", -1, 0, True),
+)
+
+
+def measure_resident(pool, precision, summation, skin, sort_every, freeze, steps, warmup, local=0):
+    """Device time per resident step (CUDA events on the context stream) of one
+    configuration; counters and step kinds of the timed steps."""
+    import torch
+    from paper_2105_00039_b200 import _native
+    ctx = _native.Context(local, pool.dtype)
+    ctx.set_option(_native.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[summation])
+    ctx.set_option(_native.CG_OPT_LIST_SKIN, skin)
+    ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+    flags_for = lambda k: ((_native.CG_STEP_SORT if sort_every > 0 and k % sort_every == 0 else 0)
+                           | (_native.CG_STEP_FREEZE if freeze else 0))
+    params = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
+    for k in range(warmup):
+        ctx.step(params, None, 1 << 24, flags_for(k))
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.synchronize()
+    ev0.record(stream)
+    ids = [ctx.step(params, None, 1 << 24, flags_for(warmup + k), wait=False) for k in range(steps)]
+    ev1.record(stream)
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    stats = [ctx.fetch_stats(i) for i in ids]
+    ctx.close()
+    kinds = {}
+    for s_ in stats:
+        kinds.setdefault(int(s_.sweep_kind), []).append(float(s_.t_force_ms))
+    mix = {{0: "grid_sweep", 1: "grid_sweep_list_build", 2: "list_sweep"}[k]:
+           {"steps": len(v), "mean_ms": float(np.mean(v))} for k, v in sorted(kinds.items())}
+    evals = float(np.mean([s.force_evals for s in stats]))
+    cands = float(np.mean([s.candidates for s in stats]))
+    return ms, evals, cands, mix
+
+
+def run_extras(args, c4_pool, local):
+    peak, _ = measured_hbm_peak()
+    out = {}
+    pools = {}
+    for key, cfg, prec, summ, skin, sort_every, freeze in EXTRAS:
+        if args.precision != "fp64" and cfg == "c4":
+            continue
+        if cfg == "c4" and prec == args.precision and args.side == 256:
+            pool, desc = c4_pool, "C4"
+        else:
+            if (cfg, prec) not in pools:
+                pools = {(cfg, prec): make_pool(cfg, prec, side=args.side)}   # keep one host pool at a time
+            pool, desc = pools[(cfg, prec)]
+        ms, evals, cands, mix = measure_resident(pool, prec, summ, skin, sort_every, freeze, 10, 3, local)
+        n = pool.count
+        fv = fp64_view(cands, evals, ms)
+        out[key] = {"workload": desc, "agents": n, "precision": prec, "summation": summ,
+                    "lists": "off" if skin == 0 else "auto", "sort_every": sort_every, "freeze": freeze,
+                    "ms_per_step": ms, "agent_updates_per_s": n / (ms * 1e-3),
+                    "pair_interactions_per_s": evals / (ms * 1e-3),
+                    "step_roofline_frac": n * B_ALG[prec] / (ms * 1e-3) / 1e9 / peak,
+                    "fp64_view_frac": fv["frac"] if fv and prec == "fp64" else None,
+                    "sweep_mix": mix}
+    return out
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def main():
     args = parse()
+    maybe_relaunch(args)
     rank, world, local = dist_init(args)
+    if args.launch_check:
+        barrier(world)
+        if rank == 0:
+            print(json.dumps({"launch_check": True, "n_gpus": world, "impl": args.impl,
+                              "parallelism": "x-slabs x%d over %s" % (world, args.exchange) if world > 1
+                              else "single GPU"}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -389,7 +517,7 @@ def main():
     from paper_2105_00039_b200.pool import PrecisionMode
 
     torch.cuda.set_device(local)
-    pool, desc = make_pool(args.config, args.precision, rank, world)
+    pool, desc = make_pool(args.config, args.precision, rank, world, args.side)
     n = pool.count
     flags_for = lambda k: ((_native.CG_STEP_SORT if args.sort_every > 0 and k % args.sort_every == 0 else 0)
                            | (_native.CG_STEP_FREEZE if args.freeze else 0))
@@ -469,11 +597,15 @@ def main():
                "h2d_bytes_per_step": n * (5 * es + 8), "d2h_bytes_per_step": d2h,
                "ms_per_step": t_e2e * 1e3, "api": "engine.step(pool, SimulationConfig(strategy=Gpu()))"}
 
+    extras = None
+    if world == 1 and args.config == "c4" and not args.no_extras:
+        extras = run_extras(args, pool, local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cp, _ = make_pool(args.config, args.precision)
+        cp, _ = make_pool(args.config, args.precision, side=args.side)
         t_med, th = cpu_port_run(cp, args.precision, args.cpu_steps, args.sort_every, args.freeze)
-        cpu = {"value": cp.count / t_med, "unit": UNIT, "cores": th, "kind": "port",
+        cpu = {"value": cp.count / t_med, "unit": UNIT, "cores": th, "kind": "port", "cpu_model": cpu_model(),
                "sample": "%d full step(s) of the same %d-agent workload, median" % (args.cpu_steps, cp.count)}
 
     if rank != 0:
@@ -501,6 +633,7 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
+        "extra": extras,
     }
     print(json.dumps(line), flush=True)
 

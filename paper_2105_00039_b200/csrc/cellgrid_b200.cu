@@ -32,7 +32,6 @@
 #include <string>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
 
 #include "../../include/cellgrid_b200.h"
 
@@ -194,11 +193,13 @@ struct cg_context {
         int64_t ref_total = 0;
         int *ref_list = nullptr;             // owned indices, grouped by (destination, kind)
         unsigned long long *ref_off = nullptr;
-        uint64_t *g_uid = nullptr, *g_uid_sorted = nullptr, *r_uid = nullptr, *r_uid_sorted = nullptr;
-        int *g_idx = nullptr, *g_idx_sorted = nullptr, *r_ord = nullptr, *r_ord_sorted = nullptr;
-        void *sort_tmp = nullptr;
-        size_t sort_tmp_bytes = 0;
-        unsigned *mismatch = nullptr;
+        uint64_t *hkey = nullptr;    // ghost table: uid -> ghost index (slab.cuh), per list epoch
+        int *hval = nullptr;
+        int64_t hcap = 0;            // slots (power of two)
+        unsigned hmask = 0;
+        int *r2g = nullptr;          // receive position -> ghost index (valid after the epoch's first refresh)
+        bool r2g_valid = false;
+        unsigned *mismatch = nullptr;   // refresh records without a ghost (read back with the next bbox)
         int64_t list_cap = 0;
     } slab;
     std::string err;
@@ -423,14 +424,13 @@ static int materialize_presentation(cg_context *c, cudaStream_t st = nullptr)
         c->table_dims[1] = g.dimy;
         c->table_dims[2] = g.dimz;
     }
-    // scratch: u64 keys x2, u32 keys x2, int values x2, + cub temp
-    size_t t1 = 0, t2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t *)nullptr, (uint64_t *)nullptr,
-                                    (const int *)nullptr, (int *)nullptr, n, 0, 64, st);
-    cub::DeviceRadixSort::SortPairs(nullptr, t2, (const unsigned *)nullptr, (unsigned *)nullptr,
-                                    (const int *)nullptr, (int *)nullptr, n, 0, 32, st);
-    const size_t tb = (std::max(t1, t2) + 255) & ~size_t(255);
-    const size_t need = (size_t)n * (8 + 4 + 4 + 4) + tb + 1024;
+    // scratch: per agent box rank, slot in box, segment entry; per Morton rank
+    // counts and offsets; the scan's tile sums; the crowded-box list
+    const int nb = g.nb;
+    const int ntiles = cdiv(nb, kScanTile);
+    auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+    const size_t need = 3 * al(sizeof(int) * (size_t)n) + 2 * al(sizeof(int) * ((size_t)nb + 1)) +
+                        al(sizeof(int) * (size_t)ntiles) + al(sizeof(int) * (size_t)n) + 256;
     if (need > c->b.pscratch_bytes) {
         if (c->b.pscratch) cudaFree(c->b.pscratch);
         c->b.pscratch = nullptr;
@@ -438,25 +438,24 @@ static int materialize_presentation(cg_context *c, cudaStream_t st = nullptr)
         c->b.pscratch_bytes = need;
     }
     char *p = (char *)c->b.pscratch;
-    uint64_t *ukeys = (uint64_t *)p;  p += (size_t)n * 8;
-    int *vals0 = (int *)p;            p += (size_t)n * 4;
-    int *vals1 = (int *)p;            p += (size_t)n * 4;
-    unsigned *mk = (unsigned *)p;     p += (size_t)n * 4;
-    p = (char *)(((uintptr_t)p + 255) & ~uintptr_t(255));
-    void *temp = p;
-    // 1. uid order (uids are unique; the stage buffer holds the sorted keys)
-    iota<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, vals0);
-    size_t tt = tb;
-    CUDA_TRY(c, cub::DeviceRadixSort::SortPairs(temp, tt, c->b.uid[c->cur_attr], ukeys, vals0, vals1, n, 0, 64, st));
-    // 2. stable by Morton rank of the box at the sort step
-    morton_keys<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, vals1, c->b.pkey[c->cur_attr], c->mrank, mk);
-    int bits = 1;
-    while (bits < 31 && (1ll << bits) < (long long)g.nb) ++bits;
-    tt = tb;
-    CUDA_TRY(c, cub::DeviceRadixSort::SortPairs(temp, tt, mk, (unsigned *)ukeys, vals1, vals0, n, 0, bits, st));
-    invert_perm<<<cdiv(n, kThreads), kThreads, 0, st>>>(n, vals0, c->b.pres);
+    auto take = [&](size_t bytes) { char *q = p; p += al(bytes); return (int *)q; };
+    int *rkey = take(sizeof(int) * (size_t)n), *slot = take(sizeof(int) * (size_t)n);
+    int *seg = take(sizeof(int) * (size_t)n);
+    int *cnt = take(sizeof(int) * ((size_t)nb + 1)), *off = take(sizeof(int) * ((size_t)nb + 1));
+    int *tsum = take(sizeof(int) * (size_t)ntiles), *big = take(sizeof(int) * (size_t)n);
+    unsigned *nbig = (unsigned *)take(256);
+    const int blk = cdiv(n, kThreads);
+    CUDA_TRY(c, cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)nb + 1), st));
+    CUDA_TRY(c, cudaMemsetAsync(nbig, 0, sizeof(unsigned), st));
+    pres_count<<<blk, kThreads, 0, st>>>(n, c->b.pkey[c->cur_attr], c->mrank, cnt, rkey, slot);
+    scan_reduce<<<ntiles, kThreads, 0, st>>>(nb, cnt, tsum);
+    scan_tilesums<<<1, 1024, 0, st>>>(ntiles, tsum);
+    scan_down<<<ntiles, kThreads, 0, st>>>(nb, cnt, tsum, off, nullptr);
+    pres_scatter<<<blk, kThreads, 0, st>>>(n, rkey, slot, off, seg);
+    pres_rank<<<blk, kThreads, 0, st>>>(n, rkey, slot, off, seg, c->b.uid[c->cur_attr], c->b.pres, big, nbig);
+    pres_rank_big<<<c->sms, 1024, 0, st>>>(big, nbig, off, seg, c->b.uid[c->cur_attr], c->b.pres);
     LAUNCH_CHECK(c);
-    c->launches += 5;
+    c->launches += 7;
     c->pres_state = PRES_VALID;
     return CG_OK;
 }
@@ -467,7 +466,8 @@ static int ensure_big(cg_context *c);
 static int ensure_lists(cg_context *c, int width);
 static int list_width_for(const cg_context *c, const Geometry &g, double skin);
 template <typename T>
-static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort, int rot = 0);
+static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort, int rot = 0,
+                          bool step_path = true);
 
 template <typename T>
 static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, bool sort,
@@ -482,12 +482,15 @@ static int build_grid(cg_context *c, double ir, int64_t box_cap, bool relayout, 
     }
     Geometry g;
     if ((rc = host_geometry(c, c->bbox_host, ir, box_cap, g, dims64, origin))) return rc;
-    return build_grid_geo<T>(c, g, relayout, sort);
+    return build_grid_geo<T>(c, g, relayout, sort, 0, false);   // a grid-only build (cg_build_grid)
 }
 
-// Grid rebuild for a given geometry (global, or a slab's sub-grid).
+// Grid rebuild for a given geometry (global, or a slab's sub-grid).  On the
+// step path (not a grid-only cg_build_grid) a dense grid also allocates the
+// warp sweep's queues and the lists a later build will need, so no build
+// step pays a cudaMalloc.
 template <typename T>
-static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort, int rot)
+static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool sort, int rot, bool step_path)
 {
     const int n = (int)c->n;
     cudaStream_t st = c->stream;
@@ -548,8 +551,8 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
         c->launches += 1;
     }
     c->last_dense = dense;
-    if (dense && (rc = ensure_big(c))) return rc;   // the warp sweep's second-pass queues
-    if (dense && c->list_skin != 0.0 && c->sweep_impl == 1 && c->n > 1) {
+    if (step_path && dense && (rc = ensure_big(c))) return rc;   // the warp sweep's second-pass queues
+    if (step_path && dense && c->list_skin != 0.0 && c->sweep_impl == 1 && c->n > 1) {
         // the lists a later build will need, allocated now (outside the build step)
         const int w = list_width_for(c, g, c->list_skin < 0 ? 0.07 * g.L : c->list_skin);
         if (w > 0 && (rc = ensure_lists(c, w))) return rc;
@@ -828,6 +831,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
 static int ensure_lists(cg_context *c, int width)
 {
     if (c->nbr && c->nbr_cap == c->cap && c->nbr_width >= width) return CG_OK;
+    c->list_valid = false;   // new storage: whatever lists there were are gone
     if (c->nbr) cudaFree(c->nbr);
     if (c->nbr_n) cudaFree(c->nbr_n);
     c->nbr = c->nbr_n = nullptr;
@@ -1205,24 +1209,37 @@ static int slab_list_alloc(cg_context *c)
 {
     auto &S = c->slab;
     if (S.list_cap >= c->cap && S.ref_list) return CG_OK;
-    void *ptrs[] = {S.ref_list, S.ref_off, S.g_uid, S.g_uid_sorted, S.r_uid, S.r_uid_sorted, S.g_idx,
-                    S.g_idx_sorted, S.r_ord, S.r_ord_sorted, S.sort_tmp, S.mismatch};
+    void *ptrs[] = {S.ref_list, S.ref_off, S.r2g, S.mismatch};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     const size_t n = (size_t)std::max<int64_t>(c->cap, 1);
     CUDA_TRY(c, cudaMalloc(&S.ref_list, sizeof(int) * n));
     CUDA_TRY(c, cudaMalloc(&S.ref_off, sizeof(unsigned long long) * kHist));
-    uint64_t **u64[] = {&S.g_uid, &S.g_uid_sorted, &S.r_uid, &S.r_uid_sorted};
-    for (uint64_t **p : u64) CUDA_TRY(c, cudaMalloc(p, sizeof(uint64_t) * n));
-    int **i32[] = {&S.g_idx, &S.g_idx_sorted, &S.r_ord, &S.r_ord_sorted};
-    for (int **p : i32) CUDA_TRY(c, cudaMalloc(p, sizeof(int) * n));
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const uint64_t *)nullptr, (uint64_t *)nullptr,
-                                    (const int *)nullptr, (int *)nullptr, (int)n, 0, 64, c->stream);
-    CUDA_TRY(c, cudaMalloc(&S.sort_tmp, tb));
-    S.sort_tmp_bytes = tb;
+    CUDA_TRY(c, cudaMalloc(&S.r2g, sizeof(int) * n));
     CUDA_TRY(c, cudaMalloc(&S.mismatch, sizeof(unsigned)));
+    CUDA_TRY(c, cudaMemsetAsync(S.mismatch, 0, sizeof(unsigned), c->stream));
     S.list_cap = c->cap;
+    return CG_OK;
+}
+
+// the ghost table's slots: a power of two >= 2 x ghosts
+static int slab_hash_alloc(cg_context *c, int64_t ng)
+{
+    auto &S = c->slab;
+    int64_t h = 1024;
+    while (h < 2 * ng) h *= 2;
+    if (h > S.hcap) {
+        if (S.hkey) cudaFree(S.hkey);
+        if (S.hval) cudaFree(S.hval);
+        S.hkey = nullptr;
+        S.hval = nullptr;
+        S.hcap = 0;
+        CUDA_TRY(c, cudaMalloc(&S.hkey, sizeof(uint64_t) * (size_t)h));
+        CUDA_TRY(c, cudaMalloc(&S.hval, sizeof(int) * (size_t)h));
+        S.hcap = h;
+    }
+    S.hmask = (unsigned)(h - 1);
+    CUDA_TRY(c, cudaMemsetAsync(S.hval, 0xff, sizeof(int) * (size_t)h, c->stream));   // -1: empty
     return CG_OK;
 }
 
@@ -1417,23 +1434,21 @@ static int slab_unpack_t(cg_context *c, const void *recv, const int64_t *rc3)
             return fail(c, CG_ERR_STATE, "ghost refresh brought %lld records for %lld ghosts", (long long)got,
                         (long long)ng);
         if (ng == 0) return CG_OK;
+        // the runs arrive in the same order all epoch: match by uid once, then
+        // scatter through r2g; a record without its ghost counts in
+        // S.mismatch, checked with the next bbox readback (no sync here)
         cudaStream_t st = c->stream;
-        const int rb = (int)sizeof(SlabRecord<T>);
-        slab_recv_keys<<<cdiv(ng, kThreads), kThreads, 0, st>>>((int)ng, (const unsigned char *)recv, rb,
-                                                                 (int)offsetof(SlabRecord<T>, uid), S.r_uid, S.r_ord);
-        size_t tb = S.sort_tmp_bytes;
-        CUDA_TRY(c, cub::DeviceRadixSort::SortPairs(S.sort_tmp, tb, S.r_uid, S.r_uid_sorted, S.r_ord, S.r_ord_sorted,
-                                                    (int)ng, 0, 64, st));
-        CUDA_TRY(c, cudaMemsetAsync(S.mismatch, 0, sizeof(unsigned), st));
-        slab_refresh_scatter<T><<<cdiv(ng, kThreads), kThreads, 0, st>>>(
-            (int)ng, (const SlabRecord<T> *)recv, S.r_ord_sorted, S.r_uid_sorted, S.g_uid_sorted, S.g_idx_sorted,
-            (Rec<T> *)c->b.rec[c->cur_pos] - S.rot_build, S.mismatch);
+        Rec<T> *rec = (Rec<T> *)c->b.rec[c->cur_pos] - S.rot_build;
+        if (!S.r2g_valid) {
+            slab_refresh_match<T><<<cdiv(ng, kThreads), kThreads, 0, st>>>(
+                (int)ng, (const SlabRecord<T> *)recv, S.hkey, S.hval, S.hmask, S.r2g, rec, S.mismatch);
+            S.r2g_valid = true;
+        } else {
+            slab_refresh_apply<T><<<cdiv(ng, kThreads), kThreads, 0, st>>>(
+                (int)ng, (const SlabRecord<T> *)recv, S.r2g, cols_at<T>(c, S.rot_build).uid, rec, S.mismatch);
+        }
         LAUNCH_CHECK(c);
-        c->launches += 3;
-        unsigned bad = 0;
-        CUDA_TRY(c, cudaMemcpyAsync(&bad, S.mismatch, sizeof bad, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(c, cudaStreamSynchronize(st));
-        if (bad) return fail(c, CG_ERR_STATE, "ghost refresh: %u records do not match the ghost set", bad);
+        c->launches += 1;
         return CG_OK;
     }
     int64_t mig = 0, glo = 0, ghi = 0;
@@ -1489,11 +1504,10 @@ static int slab_list_tables(cg_context *c)
     const int W = S.world, lo = c->rot, no = (int)c->n_owned, nt = (int)c->n;
     const int ng = nt - no;
     const SlabCols<T> C = cols_at<T>(c, lo);   // the build positions (before this step's move)
+    S.r2g_valid = false;
     if (ng > 0) {
-        slab_ghost_table<<<cdiv(ng, kThreads), kThreads, 0, st>>>(nt, lo, no, C.uid, S.g_uid, S.g_idx);
-        size_t tb = S.sort_tmp_bytes;
-        CUDA_TRY(c, cub::DeviceRadixSort::SortPairs(S.sort_tmp, tb, S.g_uid, S.g_uid_sorted, S.g_idx, S.g_idx_sorted,
-                                                    ng, 0, 64, st));
+        if ((rc = slab_hash_alloc(c, ng))) return rc;
+        slab_ghost_hash<<<cdiv(ng, kThreads), kThreads, 0, st>>>(nt, lo, no, C.uid, S.hkey, S.hval, S.hmask);
     }
     CUDA_TRY(c, cudaMemsetAsync(S.counts, 0, sizeof(unsigned long long) * kHist, st));
     if (no > 0)
@@ -1737,13 +1751,22 @@ int cg_create(int device, int precision, cg_context **out)
     c->sms = prop.multiProcessorCount;
     c->prec = precision;
     c->esz = precision == CG_FP64 ? 8 : 4;
-    // test hook: CG_LIST_SKIN_DEFAULT (same units as CG_OPT_LIST_SKIN) sets the
-    // initial neighbour-list skin of every new context
-    if (const char *e = std::getenv("CG_LIST_SKIN_DEFAULT")) {
-        const int v = std::atoi(e);
-        c->list_skin = v < 0 ? -1.0 : v * 1e-3;
-    }
     int rc = CG_OK;
+    // test hook: CG_LIST_SKIN_DEFAULT sets the initial neighbour-list skin of
+    // every new context, in LENGTH units ("auto" or a negative value = auto,
+    // 0 = lists off); anything else is refused rather than guessed
+    if (const char *e = std::getenv("CG_LIST_SKIN_DEFAULT")) {
+        char *end = nullptr;
+        const double v = std::strtod(e, &end);
+        if (std::strcmp(e, "auto") == 0) {
+            c->list_skin = -1.0;
+        } else if (end == e || *end != '\0' || !std::isfinite(v)) {
+            rc = fail(c, CG_ERR_VALUE, "CG_LIST_SKIN_DEFAULT='%s' is not a length (e.g. 0.7, 0, auto)", e);
+            std::fprintf(stderr, "cellgrid_b200: %s\n", c->err.c_str());
+        } else {
+            c->list_skin = v < 0 ? -1.0 : v;
+        }
+    }
     auto chk = [&](cudaError_t e) {
         if (e != cudaSuccess && rc == CG_OK) rc = fail(c, CG_ERR_CUDA, "%s", cudaGetErrorString(e));
     };
@@ -1777,6 +1800,13 @@ void cg_destroy(cg_context *c)
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_agents(c);
+    {
+        auto &S = c->slab;
+        void *sp[] = {S.dest, S.out, S.holes, S.movers, S.cnt, S.counts, S.seg_off, S.cursor,
+                      S.ref_list, S.ref_off, S.r2g, S.mismatch, S.hkey, S.hval};
+        for (void *p : sp)
+            if (p) cudaFree(p);
+    }
     int *ptrs[] = {c->count, c->offset, c->mrank, c->minv, c->count_own};
     for (int *p : ptrs)
         if (p) cudaFree(p);
@@ -2250,11 +2280,16 @@ int cg_local_bbox(cg_context *c, double out[9])
         return CG_OK;
     }
     int rc = CG_OK;
+    unsigned bad = 0;
+    if (c->slab.mismatch)   // ghost refreshes of the last step (slab_unpack_t)
+        CUDA_TRY(c, cudaMemcpyAsync(&bad, c->slab.mismatch, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
     if (!c->bbox_valid)
         rc = c->prec == CG_FP64 ? standalone_bbox<double>(c) : standalone_bbox<float>(c);
     else
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (rc) return rc;
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (bad) return fail(c, CG_ERR_STATE, "ghost refresh: %u records did not match the ghost set", bad);
     for (int k = 0; k < 6; ++k) out[k] = c->bbox_host[k];
     out[6] = c->max_diam;
     // the last step's largest squared displacement and neighbour-list

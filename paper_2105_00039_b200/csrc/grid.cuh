@@ -752,6 +752,82 @@ __global__ void morton_keys(int n, const int *__restrict__ order, const int *__r
     if (r < n) out[r] = (unsigned)__ldg(mrank + pkey[order[r]]);
 }
 
+// ---------------------------------------------------------------- presentation order
+// The reference's storage order after a sort step (morton.py:67-74,
+// pool.py:228-239): ascending (Morton code of the agent's box, uid).  A
+// counting sort by the box's Morton rank (pres_count -> scan -> pres_scatter)
+// puts every box's agents in one segment; inside a segment an agent's place
+// is the number of segment members with a smaller uid (pres_rank; boxes hold
+// a handful of agents, the few crowded ones take pres_rank_big: one CTA per
+// segment, uids staged through shared memory).  pres[a] = reference
+// position of storage index a.
+constexpr int kPresSmallSeg = 256;
+
+__global__ void __launch_bounds__(kThreads) pres_count(int n, const int *__restrict__ pkey,
+                                                       const int *__restrict__ mrank, int *__restrict__ cnt,
+                                                       int *__restrict__ rkey, int *__restrict__ slot)
+{
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    const int r = __ldg(mrank + __ldg(pkey + a));
+    rkey[a] = r;
+    slot[a] = atomicAdd(cnt + r, 1);
+}
+
+__global__ void __launch_bounds__(kThreads) pres_scatter(int n, const int *__restrict__ rkey,
+                                                         const int *__restrict__ slot, const int *__restrict__ off,
+                                                         int *__restrict__ seg)
+{
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < n) seg[__ldg(off + rkey[a]) + slot[a]] = a;
+}
+
+__global__ void __launch_bounds__(kThreads) pres_rank(int n, const int *__restrict__ rkey,
+                                                      const int *__restrict__ slot, const int *__restrict__ off,
+                                                      const int *__restrict__ seg, const uint64_t *__restrict__ uid,
+                                                      int *__restrict__ pres, int *__restrict__ big,
+                                                      unsigned *__restrict__ nbig)
+{
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    const int r = rkey[a];
+    const int s0 = __ldg(off + r), s1 = __ldg(off + r + 1);
+    if (s1 - s0 > kPresSmallSeg) {   // crowded box: one CTA sorts it (listed once, by its slot-0 agent)
+        if (slot[a] == 0) big[atomicAdd(nbig, 1u)] = r;
+        return;
+    }
+    const uint64_t u = uid[a];
+    int rank = 0;
+    for (int p = s0; p < s1; ++p) rank += uid[__ldg(seg + p)] < u;
+    pres[a] = s0 + rank;
+}
+
+__global__ void __launch_bounds__(1024) pres_rank_big(const int *__restrict__ big, const unsigned *__restrict__ nbig,
+                                                      const int *__restrict__ off, const int *__restrict__ seg,
+                                                      const uint64_t *__restrict__ uid, int *__restrict__ pres)
+{
+    __shared__ uint64_t tile[1024];
+    for (unsigned b = blockIdx.x; b < *nbig; b += gridDim.x) {
+        const int r = big[b];
+        const int s0 = off[r], s1 = off[r + 1];
+        for (int base = s0; base < s1; base += blockDim.x) {   // this thread's agent: seg[base + tid]
+            const int p = base + threadIdx.x;
+            const int a = p < s1 ? seg[p] : -1;
+            const uint64_t u = a >= 0 ? uid[a] : 0;
+            int rank = 0;
+            for (int t0 = s0; t0 < s1; t0 += blockDim.x) {   // uids of the segment, one tile at a time
+                __syncthreads();
+                if (t0 + (int)threadIdx.x < s1) tile[threadIdx.x] = uid[seg[t0 + threadIdx.x]];
+                __syncthreads();
+                const int m = min((int)blockDim.x, s1 - t0);
+                for (int q = 0; q < m; ++q) rank += tile[q] < u;
+            }
+            if (a >= 0) pres[a] = s0 + rank;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void invert_perm(int n, const int *__restrict__ order, int *__restrict__ pres)
 {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;

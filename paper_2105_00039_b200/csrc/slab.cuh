@@ -220,17 +220,42 @@ __global__ void slab_unpack_segs(int total, SlabSegs S, const SlabRecord<T> *__r
 // records.  Indices are the build step's (relaid) indices; the buffers are
 // addressed at index - rot (lo ghosts in the front headroom).
 
-// ghost table: the ghost indices [0, lo) U [lo + n_owned, n_total) with their
-// uids (sorted afterwards, so refresh records can be matched by uid)
-__global__ void slab_ghost_table(int n_total, int lo, int n_owned, const uint64_t *__restrict__ uid,
-                                 uint64_t *__restrict__ g_uid, int *__restrict__ g_idx)
+// ghost table: a hash map uid -> ghost index over [0, lo) U [lo + n_owned,
+// n_total) (open addressing, linear probing; a slot is claimed through its
+// value word, -1 = empty), so refresh records can be matched by uid without
+// sorting.  Built once per list epoch.
+__device__ __forceinline__ unsigned uid_hash(uint64_t u, unsigned mask)
+{
+    u ^= u >> 33;
+    u *= 0xff51afd7ed558ccdULL;
+    u ^= u >> 33;
+    return (unsigned)u & mask;
+}
+
+__global__ void slab_ghost_hash(int n_total, int lo, int n_owned, const uint64_t *__restrict__ uid,
+                                uint64_t *__restrict__ hkey, int *__restrict__ hval, unsigned mask)
 {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int ng = n_total - n_owned;
     if (k >= ng) return;
     const int i = k < lo ? k : k + n_owned;
-    g_uid[k] = uid[i];
-    g_idx[k] = i;
+    const uint64_t u = uid[i];
+    for (unsigned h = uid_hash(u, mask);; h = (h + 1) & mask) {
+        if (atomicCAS(hval + h, -1, i) == -1) {
+            hkey[h] = u;
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ int ghost_lookup(const uint64_t *__restrict__ hkey, const int *__restrict__ hval,
+                                            unsigned mask, uint64_t u)
+{
+    for (unsigned h = uid_hash(u, mask);; h = (h + 1) & mask) {
+        const int v = hval[h];
+        if (v < 0) return -1;
+        if (hkey[h] == u) return v;
+    }
 }
 
 // refresh lists: owned agents in another rank's ghost band (at the build
@@ -263,35 +288,51 @@ __global__ void slab_refresh_pack(int count, const int *__restrict__ list, SlabC
     out[k] = r;
 }
 
-__global__ void slab_recv_keys(int count, const unsigned char *__restrict__ recv, int rec_bytes, int uid_off,
-                               uint64_t *__restrict__ keys, int *__restrict__ vals)
-{
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= count) return;
-    keys[k] = *reinterpret_cast<const uint64_t *>(recv + (size_t)k * rec_bytes + uid_off);
-    vals[k] = k;
-}
-
-// the p-th received record (by uid) refreshes the p-th ghost (by uid)
+// the first refresh of a list epoch: every received record finds its ghost
+// by uid (r2g remembers it: the runs arrive in the same order every step of
+// the epoch); later refreshes only check the uid (slab_refresh_apply).
+// Unmatched records count in *mismatch, read back with the next bbox.
 template <typename T>
-__global__ void slab_refresh_scatter(int count, const SlabRecord<T> *__restrict__ in, const int *__restrict__ order,
-                                     const uint64_t *__restrict__ got_uid, const uint64_t *__restrict__ want_uid,
-                                     const int *__restrict__ g_idx, Rec<T> *__restrict__ rec,
-                                     unsigned *__restrict__ mismatch)
+__global__ void slab_refresh_match(int count, const SlabRecord<T> *__restrict__ in, const uint64_t *__restrict__ hkey,
+                                   const int *__restrict__ hval, unsigned mask, int *__restrict__ r2g,
+                                   Rec<T> *__restrict__ rec, unsigned *__restrict__ mismatch)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= count) return;
-    if (got_uid[p] != want_uid[p]) {
+    const SlabRecord<T> r = in[p];
+    const int g = ghost_lookup(hkey, hval, mask, r.uid);
+    r2g[p] = g;
+    if (g < 0) {
         atomicAdd(mismatch, 1u);
         return;
     }
-    const SlabRecord<T> r = in[order[p]];
     Rec<T> v;
     v.x = r.v[0];
     v.y = r.v[1];
     v.z = r.v[2];
     v.d = r.v[3];
-    rec[g_idx[p]] = v;
+    rec[g] = v;
+}
+
+template <typename T>
+__global__ void slab_refresh_apply(int count, const SlabRecord<T> *__restrict__ in, const int *__restrict__ r2g,
+                                   const uint64_t *__restrict__ uid, Rec<T> *__restrict__ rec,
+                                   unsigned *__restrict__ mismatch)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= count) return;
+    const SlabRecord<T> r = in[p];
+    const int g = r2g[p];
+    if (g < 0 || uid[g] != r.uid) {
+        atomicAdd(mismatch, 1u);
+        return;
+    }
+    Rec<T> v;
+    v.x = r.v[0];
+    v.y = r.v[1];
+    v.z = r.v[2];
+    v.d = r.v[3];
+    rec[g] = v;
 }
 
 }  // namespace cg
