@@ -141,6 +141,23 @@ int cg_force_phase(cg_context *ctx, int64_t n, const void *px, const void *py, c
                    const void *params7, void *out_dx, void *out_dy, void *out_dz,
                    int64_t counters[3]);
 
+/* ---- behaviour phase: engine.grow_and_divide
+ * (engine.py:191-232) on the resident pool, before the step.  Every agent's
+ * volume pi/6 d^3 grows by volume_growth_rate (pool dtype), d = cbrt(volume /
+ * (pi/6)); with division_enabled, agents with d >= division_diameter split in
+ * ascending uid: both halves get d = cbrt(half volume / (pi/6)), the daughter
+ * is placed at mother radius / 4 along rng.unit_vector(uid, step_index)
+ * (rng.py:41-54) and appended (pool.py:199-217 append_many) with uid next_uid +
+ * rank, zero displacement, the mother's adherence.  cbrt is numpy's SVML
+ * routine and the direction numpy's Philox + ziggurat, restated bit for bit
+ * (csrc/behavior_math.h).  *divisions receives the number of divisions; the
+ * caller advances its next_uid by it.  The pool grows in place (capacity is
+ * extended as needed); the storage order of existing agents is unchanged. */
+int cg_behavior(cg_context *ctx, int64_t step_index, double volume_growth_rate, double division_diameter,
+                int division_enabled, uint64_t next_uid, int64_t *divisions);
+/* rng.unit_vector(uid[i], step) for n uids (rng.py:41-54): out is n x 3 f64. */
+int cg_unit_vectors(cg_context *ctx, int64_t n, const uint64_t *uid, int64_t step, double *out);
+
 /* Neighbour-list reuse counters (CG_OPT_LIST_SKIN): out[0] list builds,
  * out[1] steps served from lists, out[2] lists currently valid, out[3] skin of
  * the last build in 1e-6 length units. */

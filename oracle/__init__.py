@@ -6,8 +6,9 @@ Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
 reference functions and DESIGN.md ("Oracle") for how it is pinned.
 """
 
+from . import behavior
 from .oracle import (OracleError, OracleGridOverflow, OracleStep, all_pairs, box_ids,
                      build, csr, force_phase, geometry, lib, morton_encode, morton_perm, neighbor_csr, step)
 
-__all__ = ["OracleError", "OracleGridOverflow", "OracleStep", "all_pairs", "box_ids", "build",
+__all__ = ["behavior", "OracleError", "OracleGridOverflow", "OracleStep", "all_pairs", "box_ids", "build",
            "csr", "force_phase", "geometry", "lib", "morton_encode", "morton_perm", "step"]

@@ -31,7 +31,8 @@ EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_
             "cg_host_alloc", "cg_host_free", "cg_record_bytes", "cg_reserve", "cg_local_bbox",
             "cg_slab_plan", "cg_slab_pack", "cg_slab_unpack",
             "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill",
-            "cg_list_stats", "cg_slab_list_epoch", "cg_step_download")
+            "cg_list_stats", "cg_slab_list_epoch", "cg_step_download", "cg_behavior",
+            "cg_unit_vectors")
 
 
 class GridOverflowError(RuntimeError):
@@ -100,6 +101,9 @@ def load():
         "cg_force_phase": ([_P, _I64] + [_P] * 7 + [_I64] * 3 + [_P] * 5, ctypes.c_int),
         "cg_neighbor_counts": ([_P, ctypes.c_double, _P], ctypes.c_int),
         "cg_list_stats": ([_P, _P], ctypes.c_int),
+        "cg_behavior": ([_P, _I64, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_uint64, _P],
+                        ctypes.c_int),
+        "cg_unit_vectors": ([_P, _I64, _P, _I64, _P], ctypes.c_int),
         "cg_step_download": ([_P, _P, ctypes.c_double, _I64, ctypes.c_int, ctypes.POINTER(StepStatsC)]
                              + [_P] * 9, ctypes.c_int),
         "cg_slab_list_epoch": ([_P], _I64),
@@ -255,6 +259,22 @@ class Context:
         bc = np.empty(num_boxes, np.int64)
         check(load().cg_grid_export(self.h, ptr(bi), ptr(bc)), self.h)
         return bi, bc
+
+    def behavior(self, step_index, volume_growth_rate, division_diameter, division_enabled, next_uid):
+        """cg_behavior: grow (and divide) the resident pool; returns the number
+        of divisions (the caller's next_uid advances by it)."""
+        out = ctypes.c_int64(0)
+        check(load().cg_behavior(self.h, int(step_index), float(volume_growth_rate), float(division_diameter),
+                                 1 if division_enabled else 0, int(next_uid), ctypes.byref(out)), self.h)
+        self.n += int(out.value)
+        return int(out.value)
+
+    def unit_vectors(self, uid, step):
+        """rng.unit_vector(uid[i], step) for every uid, on the device: (n, 3) f64."""
+        uid = np.ascontiguousarray(uid, np.uint64)
+        out = np.empty((uid.shape[0], 3), np.float64)
+        check(load().cg_unit_vectors(self.h, uid.shape[0], ptr(uid), int(step), ptr(out)), self.h)
+        return out
 
     def list_stats(self):
         """(builds, list steps, valid, skin) of the neighbour-list reuse."""

@@ -52,6 +52,7 @@
 #include "sweep_warp.cuh"
 #include "query.cuh"
 #include "list.cuh"
+#include "behavior.cuh"
 
 using namespace cg;
 
@@ -155,6 +156,8 @@ struct cg_context {
     int list_life = 0, list_backoff = 0, list_wait = 0;
     int64_t list_builds = 0, list_steps = 0;
     bool uid32 = false;           // every stored uid < 2^32 (set at upload; slab exchanges clear it)
+    void *beh = nullptr;          // behaviour phase scratch (ripe list, sort buffers), beh_bytes
+    size_t beh_bytes = 0;
     unsigned long long *maxuid_dev = nullptr;
     int rot = 0;                  // relaid slab sub-grid: slot s lives at storage s - rot (lo ghosts in
                                   // the buffers' front headroom, owned agents at [0, n_owned))
@@ -274,6 +277,49 @@ static int alloc_agents(cg_context *c, int64_t cap)
     CUDA_TRY(c, cudaMemset(b.prox, 0, sizeof(float) * 8 * (size_t)b.pairs));
     CUDA_TRY(c, cudaMalloc(&b.stage, 8 * (size_t)cap));
     c->cap = cap;
+    return CG_OK;
+}
+
+// More agent capacity with the resident pool kept: the live columns (records,
+// adherence, uid, displacements, the presentation order) move to buffers of
+// the new capacity; per-step scratch is reallocated, neighbour lists dropped.
+static int grow_agents(cg_context *c, int64_t cap)
+{
+    const Buffers old = c->b;
+    const int64_t n = c->n;
+    const int cp = c->cur_pos, ca = c->cur_attr;
+    c->b = Buffers{};   // alloc_agents frees c->b: keep the old set alive until copied
+    const int64_t oldcap = c->cap;
+    c->cap = 0;
+    int *nbr = c->nbr, *nbr_n = c->nbr_n;
+    c->nbr = c->nbr_n = nullptr;
+    int rc = alloc_agents(c, cap);
+    if (nbr) cudaFree(nbr);
+    if (nbr_n) cudaFree(nbr_n);
+    if (rc) return rc;
+    cudaStream_t st = c->stream;
+    const size_t es = c->esz;
+    CUDA_TRY(c, cudaMemcpyAsync(c->b.rec[0], old.rec[cp], 4 * es * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->b.adh[0], old.adh[ca], es * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->b.uid[0], old.uid[ca], 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    for (int a = 0; a < 3; ++a)
+        CUDA_TRY(c, cudaMemcpyAsync(c->b.disp[a], old.disp[a], es * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->b.pres, old.pres, 4 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->b.pkey[0], old.pkey[ca], 4 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    for (int k = 0; k < 2; ++k) {
+        if (old.rec[k]) cudaFree((char *)old.rec[k] - 4 * es * old.head);
+        if (old.adh[k]) cudaFree((char *)old.adh[k] - es * old.head);
+        if (old.uid[k]) cudaFree(old.uid[k] - old.head);
+    }
+    void *ptrs[] = {old.disp[0], old.disp[1], old.disp[2], old.key_rank, old.tmp, old.idx, old.skey, old.pres,
+                    old.rec_m, old.rec_nk, old.prox, old.stage, old.pkey[0], old.pkey[1], old.pscratch, old.ovf};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    (void)oldcap;
+    c->cur_pos = c->cur_attr = 0;
+    c->have_grid = false;
+    c->relaid = false;
     return CG_OK;
 }
 
@@ -1721,6 +1767,107 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
 }
 
 // --------------------------------------------------------------------------- C ABI
+// ---------------------------------------------------------------- behaviour phase
+template <typename T>
+static int behavior_t(cg_context *c, int64_t step_index, double rate, double div_d, bool divide, uint64_t next_uid,
+                      int64_t *divisions)
+{
+    *divisions = 0;
+    const int64_t n = c->n;
+    if (n == 0) return CG_OK;
+    cudaStream_t st = c->stream;
+    int rc;
+    // daughters take reference positions n, n + 1, ...: the order must be explicit
+    if ((rc = materialize_presentation(c))) return rc;
+    const int ntiles = cdiv(n, kSortTile);
+    auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+    const size_t need = 2 * al(8 * (size_t)n) + 2 * al(4 * (size_t)n) + 2 * al(4 * 256 * (size_t)ntiles + 4) +
+                        al(4 * (size_t)cdiv(256 * ntiles, kScanTile)) + 256;
+    if (need > c->beh_bytes) {
+        if (c->beh) cudaFree(c->beh);
+        c->beh = nullptr;
+        c->beh_bytes = 0;
+        CUDA_TRY(c, cudaMalloc(&c->beh, need));
+        c->beh_bytes = need;
+    }
+    char *p = (char *)c->beh;
+    auto take = [&](size_t b) { char *q = p; p += al(b); return (void *)q; };
+    uint64_t *key0 = (uint64_t *)take(8 * (size_t)n), *key1 = (uint64_t *)take(8 * (size_t)n);
+    int *idx0 = (int *)take(4 * (size_t)n), *idx1 = (int *)take(4 * (size_t)n);
+    int *hist = (int *)take(4 * 256 * (size_t)ntiles + 4), *offs = (int *)take(4 * 256 * (size_t)ntiles + 4);
+    int *tsum = (int *)take(4 * (size_t)cdiv(256 * ntiles, kScanTile));
+    unsigned *nripe = (unsigned *)take(256);
+    CUDA_TRY(c, cudaMemsetAsync(nripe, 0, sizeof(unsigned), st));
+    Rec<T> *rec = (Rec<T> *)c->b.rec[c->cur_pos];
+    grow_kernel<T><<<cdiv(n, kThreads), kThreads, 0, st>>>((int)n, rec, c->b.uid[c->cur_attr], (T)rate, (T)div_d, divide,
+                                                           key0, idx0, nripe);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    unsigned k = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&k, nripe, sizeof k, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    if (k > 0) {
+        if (n + (int64_t)k >= (int64_t)INT32_MAX / 4)
+            return fail(c, CG_ERR_POOL_CAPACITY, "%lld agents exceeds the device cap", (long long)(n + k));
+        // mothers by uid (the order daughters take uids and places in): LSD radix
+        // passes over the bytes in which the ripe uids differ
+        unsigned long long oa[2] = {0ull, ~0ull};
+        unsigned long long *doa = (unsigned long long *)(nripe + 2);
+        CUDA_TRY(c, cudaMemcpyAsync(doa, oa, sizeof oa, cudaMemcpyHostToDevice, st));
+        key_or_and<<<std::min(cdiv(k, kThreads), c->sms * 4), kThreads, 0, st>>>((int)k, key0, doa);
+        CUDA_TRY(c, cudaMemcpyAsync(oa, doa, sizeof oa, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        const uint64_t vary = oa[0] ^ oa[1];
+        const int kt = cdiv(k, kSortTile);
+        const int nh = 256 * kt;
+        for (int sh = 0; sh < 64; sh += 8) {
+            if (!((vary >> sh) & 0xff)) continue;
+            radix_hist<<<kt, kThreads, 0, st>>>((int)k, key0, sh, hist, kt);
+            const int nt = cdiv(nh, kScanTile);
+            scan_reduce<<<nt, kThreads, 0, st>>>(nh, hist, tsum);
+            scan_tilesums<<<1, 1024, 0, st>>>(nt, tsum);
+            scan_down<<<nt, kThreads, 0, st>>>(nh, hist, tsum, offs, nullptr);
+            radix_scatter<<<kt, kThreads, 0, st>>>((int)k, key0, idx0, key1, idx1, sh, offs, kt);
+            LAUNCH_CHECK(c);
+            c->launches += 5;
+            std::swap(key0, key1);
+            std::swap(idx0, idx1);
+        }
+        if (n + (int64_t)k > c->cap) {   // room for the daughters (the pool at most doubles per step)
+            const int64_t want = std::max<int64_t>(n + k, std::min<int64_t>(2 * n, (int64_t)INT32_MAX / 4 - 1));
+            // the ripe list lives in c->beh, which grow_agents leaves alone
+            if ((rc = grow_agents(c, want))) return rc;
+            rec = (Rec<T> *)c->b.rec[c->cur_pos];
+        }
+        divide_kernel<T><<<cdiv(k, kThreads), kThreads, 0, st>>>(
+            (int)k, (int)n, key0, idx0, rec, (T *)c->b.adh[c->cur_attr], c->b.uid[c->cur_attr], (T *)c->b.disp[0],
+            (T *)c->b.disp[1], (T *)c->b.disp[2], c->pres_state == PRES_VALID ? c->b.pres : nullptr, next_uid,
+            (uint64_t)step_index);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        c->n = c->n_owned = n + k;
+        const uint64_t last = next_uid + k - 1;
+        c->uid32 = c->uid32 && last < (1ull << 32);
+    }
+    // new diameters (and daughters): the largest diameter and the bbox are recomputed
+    CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, sizeof(unsigned long long), st));
+    max_diam_kernel<T><<<std::min(c->sms * 4, cdiv(c->n, kThreads)), kThreads, 0, st>>>((int)c->n, rec, c->maxd_enc);
+    LAUNCH_CHECK(c);
+    c->launches += 1;
+    unsigned long long enc = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    c->max_diam = dec_ordered(enc);
+    c->bbox_valid = false;
+    c->list_valid = false;      // lists were built for the old radii
+    c->last_kind = 0;
+    c->have_grid = false;
+    c->grid_current = false;
+    c->relaid = false;
+    *divisions = k;
+    return CG_OK;
+}
+
 extern "C" {
 
 int cg_abi_version(void) { return CG_ABI_VERSION; }
@@ -1811,7 +1958,7 @@ void cg_destroy(cg_context *c)
     for (int *p : ptrs)
         if (p) cudaFree(p);
     void *vptrs[] = {c->scan_status, c->slots, c->maxd_enc, c->ovf_count, c->block_counters, c->bbox_dev, c->stat_dev,
-                     c->maxuid_dev, c->big, c->ovf2, c->ovf2_count};
+                     c->maxuid_dev, c->big, c->ovf2, c->ovf2_count, c->beh};
     for (void *p : vptrs)
         if (p) cudaFree(p);
     if (c->bbox_host) cudaFreeHost(c->bbox_host);
@@ -2414,6 +2561,40 @@ int64_t cg_slab_list_epoch(const cg_context *c)
 {
     if (!c) return -1;
     return c->slab.planned && c->slab.list_mode ? c->list_builds : -1;
+}
+
+int cg_behavior(cg_context *c, int64_t step_index, double volume_growth_rate, double division_diameter,
+                int division_enabled, uint64_t next_uid, int64_t *divisions)
+{
+    if (!c || !divisions) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (c->n_owned != c->n) return fail(c, CG_ERR_STATE, "cg_behavior on a slab context with ghosts");
+    return c->prec == CG_FP64 ? behavior_t<double>(c, step_index, volume_growth_rate, division_diameter,
+                                                   division_enabled != 0, next_uid, divisions)
+                              : behavior_t<float>(c, step_index, volume_growth_rate, division_diameter,
+                                                  division_enabled != 0, next_uid, divisions);
+}
+
+int cg_unit_vectors(cg_context *c, int64_t n, const uint64_t *uid, int64_t step, double *out)
+{
+    if (!c || n < 0) return CG_ERR_VALUE;
+    if (n == 0) return CG_OK;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    uint64_t *du = nullptr;
+    double *dv = nullptr;
+    CUDA_TRY(c, cudaMalloc(&du, 8 * (size_t)n));
+    CUDA_TRY(c, cudaMalloc(&dv, 24 * (size_t)n));
+    cudaStream_t st = c->stream;
+    CUDA_TRY(c, cudaMemcpyAsync(du, uid, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+    unit_vector_kernel<<<cdiv(n, kThreads), kThreads, 0, st>>>((int)n, du, (uint64_t)step, dv);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, dv, 24 * (size_t)n, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(du);
+    cudaFree(dv);
+    c->launches += 1;
+    if (e != cudaSuccess) return fail(c, CG_ERR_CUDA, "cg_unit_vectors: %s", cudaGetErrorString(e));
+    return CG_OK;
 }
 
 int cg_list_stats(cg_context *c, int64_t out[4])

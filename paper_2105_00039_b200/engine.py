@@ -15,11 +15,9 @@ the pool.  ``run`` keeps the population resident in HBM for all steps and
 synchronises the host pool once at the end.
 
 The behaviour phase (growth then division, reference engine.py:191-232) runs
-on the host before the device step, with the reference's own numpy
-arithmetic: np.cbrt is the platform libm's (not correctly rounded) and the
-daughter directions are numpy's Philox / ziggurat normal draws, neither of
-which a device kernel reproduces bit for bit.  A run with
-growth therefore synchronises the pool every step.
+on the device too (cg_behavior, csrc/behavior.cuh), bit for bit: numpy's SVML
+cube root and its Philox + ziggurat daughter directions are restated in
+csrc/behavior_math.h.  A run with growth keeps the pool resident.
 """
 
 from __future__ import annotations
@@ -35,7 +33,6 @@ import numpy as np
 from . import _native
 from .mechanics import ForceParams
 from .pool import PrecisionMode
-from .rng import unit_vector
 
 RECORD_SCALARS = 5      # reference engine.py:38-39 (bytes_modeled record)
 DEFAULT_BOX_CAP = 1 << 24
@@ -201,43 +198,22 @@ def _release_contexts():
     _contexts.clear()
 
 
-_SIXTH_PI = np.pi / 6.0
-
-
-def grow_and_divide(pool, growth: GrowthParams, step_index=0):
-    """Behaviour phase (reference engine.py:191-232), host numpy: every agent's
-    volume pi/6 d^3 grows by ``volume_growth_rate`` (pool dtype); agents whose
-    diameter reached ``division_diameter`` split, mothers in ascending uid:
-    the mother keeps half the volume, the daughter (the other half, same
-    adherence) is appended at mother_radius / 4 along ``unit_vector(uid,
-    step_index)``.  Returns the number of divisions."""
+def grow_and_divide(pool, growth: GrowthParams, step_index=0, strategy=None):
+    """Behaviour phase (reference engine.py:191-232) on the device: every
+    agent's volume pi/6 d^3 grows by ``volume_growth_rate`` (pool dtype);
+    agents whose diameter reached ``division_diameter`` split, mothers in
+    ascending uid: the mother keeps half the volume, the daughter (the other
+    half, same adherence) is appended at mother_radius / 4 along
+    ``unit_vector(uid, step_index)``.  The pool is updated in place (the
+    daughters appended, next_uid advanced); returns the number of divisions."""
     if pool.count == 0:
         return 0
-    T = pool.dtype.type
-    k6 = T(_SIXTH_PI)
-    d = pool.diameter
-    vol = k6 * (d * d * d) + T(growth.volume_growth_rate)
-    pool.diameter = np.cbrt(vol / k6)
-    if not growth.division_enabled:
-        return 0
-    ripe = np.flatnonzero(pool.diameter >= T(growth.division_diameter))
-    if ripe.shape[0] == 0:
-        return 0
-    ripe = ripe[np.argsort(pool.uid[ripe])]
-    k = ripe.shape[0]
-    where = np.empty((k, 3), np.float64)
-    half_d = np.empty(k, np.float64)
-    adh = np.empty(k, np.float64)
-    for row, i in enumerate(ripe):
-        dm = pool.diameter[i]
-        dh = np.cbrt((T(0.5) * (k6 * (dm * dm * dm))) / k6)
-        shift = unit_vector(int(pool.uid[i]), step_index) * (float(dm) * 0.5 / 4.0)
-        where[row] = (float(pool.position_x[i]) + shift[0], float(pool.position_y[i]) + shift[1],
-                      float(pool.position_z[i]) + shift[2])
-        half_d[row] = float(dh)
-        adh[row] = float(pool.adherence[i])
-        pool.diameter[i] = dh
-    pool.append_many(where, half_d, adh)
+    ctx = _context(strategy or Gpu(), pool.dtype)
+    _upload(ctx, pool)
+    k = ctx.behavior(step_index, growth.volume_growth_rate, growth.division_diameter,
+                     growth.division_enabled, pool.next_uid)
+    _assign(pool, ctx.download())
+    pool.next_uid += k
     return k
 
 
@@ -321,29 +297,32 @@ def _to_stats(st, step_index, itemsize):
 
 
 def step(pool, config: SimulationConfig, step_index=0):
-    """Advance ``pool`` by one step: the behaviour phase (if configured) on the
-    host, then the mechanical step on the GPU; returns StepStats."""
+    """Advance ``pool`` by one step: the behaviour phase (if configured), then
+    the mechanical step, both on the GPU; returns StepStats."""
     _check(pool, config)
-    divisions, t_behavior = 0, 0.0
-    if config.growth is not None and pool.count:
-        t0 = time.perf_counter()
-        divisions = grow_and_divide(pool, config.growth, step_index)
-        t_behavior = time.perf_counter() - t0
     if pool.count == 0:
-        st = _empty_stats(step_index)
-        st.t_behavior = t_behavior
-        return st
+        return _empty_stats(step_index)
     ctx = _context(config.strategy, pool.dtype)
     _upload(ctx, pool)
+    divisions, t_behavior = 0, 0.0
+    if config.growth is not None:
+        t0 = time.perf_counter()
+        g = config.growth
+        divisions = ctx.behavior(step_index, g.volume_growth_rate, g.division_diameter, g.division_enabled,
+                                 pool.next_uid)
+        pool.next_uid += divisions
+        t_behavior = time.perf_counter() - t0
     # the step and the download of its result, transfers overlapped with the sweep;
-    # a step without the Z-order sort keeps the storage order, so diameter,
-    # adherence and uid on the host are already the device's
+    # a step without the Z-order sort (and without growth) keeps the storage
+    # order and the diameters, so diameter, adherence and uid on the host are
+    # already the device's
     flags = step_flags(config, step_index)
     sorted_step = bool(flags & _native.CG_STEP_SORT)
-    wanted = _POOL_KEYS if sorted_step else ("px", "py", "pz", "dx", "dy", "dz")
+    whole = sorted_step or config.growth is not None
+    wanted = _POOL_KEYS if whole else ("px", "py", "pz", "dx", "dy", "dz")
     st, cols = ctx.step_download(params_vector(config.force_params), config.interaction_radius,
                                  DEFAULT_BOX_CAP, flags, into=_reusable(ctx, pool), columns=wanted)
-    if not sorted_step:
+    if not whole:
         cols.update(diameter=pool.diameter, adherence=pool.adherence, uid=pool.uid)
     _assign(pool, cols)
     out = _to_stats(st, step_index, pool.precision.itemsize)
@@ -354,28 +333,39 @@ def step(pool, config: SimulationConfig, step_index=0):
 
 
 def run(pool, config: SimulationConfig):
-    """``config.steps`` steps with the pool resident on the device (synchronised
-    every step when the behaviour phase is on: it runs on the host)."""
+    """``config.steps`` steps with the pool resident on the device (behaviour
+    phase included); the host pool is synchronised once, at the end."""
     _check(pool, config)
     t0 = time.perf_counter()
     initial = pool.count
     stats = []
-    if config.growth is not None:
-        stats = [step(pool, config, k) for k in range(config.steps)]
-    elif pool.count == 0:
+    if pool.count == 0:
         stats = [_empty_stats(k) for k in range(config.steps)]
     elif config.steps:
         ctx = _context(config.strategy, pool.dtype)
         _upload(ctx, pool)
         pv = params_vector(config.force_params)
-        ids, raw = [], []
+        g = config.growth
+        ids, raw, divs, tbeh = [], [], [], []
         for k in range(config.steps):
+            d, tb = 0, 0.0
+            if g is not None:
+                tb0 = time.perf_counter()
+                d = ctx.behavior(k, g.volume_growth_rate, g.division_diameter, g.division_enabled, pool.next_uid)
+                pool.next_uid += d
+                tb = time.perf_counter() - tb0
+            divs.append(d)
+            tbeh.append(tb)
             ids.append(ctx.step(pv, config.interaction_radius, DEFAULT_BOX_CAP,
                                 step_flags(config, k), wait=False))
             if len(ids) > 16:                     # the device stats ring holds 64 steps
                 raw.append(ctx.fetch_stats(ids.pop(0)))
         raw.extend(ctx.fetch_stats(i) for i in ids)
         stats = [_to_stats(st, k, pool.precision.itemsize) for k, st in enumerate(raw)]
+        for s_, d, tb in zip(stats, divs, tbeh):
+            s_.divisions = d
+            s_.t_behavior = tb
+            s_.t_total += tb
         _download(ctx, pool)
     return RunReport(strategy=strategy_label(config.strategy), precision=config.precision.value,
                      initial_count=initial, final_count=pool.count, steps=stats,
