@@ -118,6 +118,7 @@ struct cg_context {
     double *bbox_dev = nullptr, *bbox_host = nullptr;
     bool bbox_valid = false;
     double max_diam = 0.0;
+    double min_diam = -INFINITY;   // == max_diam: a uniform pool (list sweep pair constants from the host)
     unsigned long long *stat_dev = nullptr, *stat_host = nullptr;
     cg_step_stats ring[kRing];
     cudaEvent_t ev[kRing][5];
@@ -616,12 +617,12 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
     return CG_OK;
 }
 
-template <typename T, bool UID, bool ZS, int KS, bool FLUSH, int MINB, bool KEY32 = false>
+template <typename T, bool UID, bool ZS, int KS, bool FLUSH, int MINB, bool KEY32 = false, bool UNI = false>
 static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
 {
     cudaStream_t st = c->stream;
     CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
-    sweep7_kernel<T, UID, ZS, KS, FLUSH, MINB, false, KEY32><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
+    sweep7_kernel<T, UID, ZS, KS, FLUSH, MINB, false, KEY32, UNI><<<cdiv(A.n, kThreads), kThreads, 0, st>>>(A);
     LAUNCH_CHECK(c);
     c->launches += 1;
     if (!FLUSH) {   // agents with more than KS survivors (none in most steps)
@@ -684,6 +685,21 @@ static int launch_sweep_warp_big(cg_context *c, const Sweep7Args<T> &A0)
     return CG_OK;
 }
 
+// Uniform fp64 pool: the sweep's pair constants (sweep7.cuh UNI), host-computed
+// with the kernel's expressions.  Sets them in a copy the caller launches with.
+template <typename T>
+static bool sweep_uniform(const cg_context *c, const Sweep7Args<T> &A0)
+{
+    Sweep7Args<T> &A = const_cast<Sweep7Args<T> &>(A0);
+    if (sizeof(T) != 8 || !(c->min_diam == c->max_diam) || !std::isfinite(c->max_diam)) return false;
+    const T ri = (T)c->max_diam * T(0.5);
+    const T rsum = ri + ri;
+    A.u_rsum = rsum;
+    A.u_req = (ri * ri) / rsum;
+    A.u_lim = rsum + A.skin;
+    return std::isnormal(A.u_req) && std::isnormal(rsum);
+}
+
 template <typename T>
 static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
 {
@@ -692,7 +708,11 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
         if (!c->last_dense) {
             const int g1 = cdiv(A.n, kThreads), g2 = std::min(cdiv(A.n, kThreads), c->sms * 2);
-            if (CG_KEY32 && A.uid32) {
+            if (CG_KEY32 && A.uid32 && sweep_uniform(c, A)) {
+                sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true, true, true>
+                    <<<g1, kThreads, 0, st>>>(A);
+                sweep7_overflow<T, true, false, 16, true, true><<<g2, kThreads, 0, st>>>(A);
+            } else if (CG_KEY32 && A.uid32) {
                 sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true, true><<<g1, kThreads, 0, st>>>(A);
                 sweep7_overflow<T, true, false, 16, true, true><<<g2, kThreads, 0, st>>>(A);
             } else {
@@ -722,6 +742,8 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         // sparse: survivors summed in uid order (deterministic and bit-identical to
         // the reference whatever the slot order in a box); agents with more than
         // 16 survivors go to the overflow kernel
+        if (CG_KEY32 && A.uid32 && sweep_uniform(c, A))
+            return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB, true, true>(c, A);
         if (CG_KEY32 && A.uid32) return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB, true>(c, A);
         return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB>(c, A);
     }
@@ -932,6 +954,36 @@ static void list_account(cg_context *c)
     }
 }
 
+// Uniform pool: the list sweep's pair constants (list.cuh UNI), in the pool
+// dtype with the kernel's expression order (host: -ffp-contract=off, SSE).
+// fp64 only (C4 list sweep 1.159 -> 1.040 ms, C3-27 0.465 -> 0.403 ms; the
+// fp32 kernel measured 0.921 -> 0.940 ms, profiles/r2/ab_r2g.jsonl).
+template <typename T>
+static bool list_uniform(const cg_context *c, ListArgs<T> &A)
+{
+    if (sizeof(T) != 8 || !(c->min_diam == c->max_diam) || !std::isfinite(c->max_diam)) return false;
+    const T ri = (T)c->max_diam * T(0.5);
+    const T rsum = ri + ri;
+    A.u_rsum = rsum;
+    A.u_req = (ri * ri) / rsum;
+    A.u_bound = rsum * rsum * (sizeof(T) == 8 ? (T)1.0000000000009095 : (T)1.00000048f);
+    return std::isnormal(A.u_req) && std::isnormal(rsum);
+}
+
+template <typename T>
+static void launch_list_sweep(cg_context *c, ListArgs<T> &A, int n, bool fused, cudaStream_t st)
+{
+    const bool uni = list_uniform<T>(c, A);
+    const int nblk = cdiv(n, kListThreads);
+    if (fused) {
+        if (uni) list_sweep_kernel<T, true, true><<<nblk, kListThreads, 0, st>>>(A);
+        else list_sweep_kernel<T, true><<<nblk, kListThreads, 0, st>>>(A);
+    } else {
+        if (uni) list_sweep_kernel<T, false, true><<<nblk, kListThreads, 0, st>>>(A);
+        else list_sweep_kernel<T><<<nblk, kListThreads, 0, st>>>(A);
+    }
+}
+
 template <typename T>
 static int list_step_t(cg_context *c, const Geometry &g, const double params[5], bool sort, bool freeze,
                        bool record)
@@ -985,13 +1037,13 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     A.slots = c->slots;
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
     if (fused) {
-        list_sweep_kernel<T, true><<<cdiv(n, kListThreads), kListThreads, 0, st>>>(A);
+        launch_list_sweep<T>(c, A, n, true, st);
         const int gb = std::min(cdiv(g.nb, kThreads), c->sms * 8);
         box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);   // offsets are unused on a fused step
         box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, nullptr, c->offset, c->slots, stat);
         c->launches += 3;
     } else {
-        list_sweep_kernel<T><<<cdiv(n, kListThreads), kListThreads, 0, st>>>(A);
+        launch_list_sweep<T>(c, A, n, false, st);
         c->launches += 1;
     }
     finish_step<<<1, kThreads, 0, st>>>(c->slots, c->max_diam, stat, c->bbox_dev,
@@ -1391,6 +1443,7 @@ static int slab_plan_t(cg_context *c, const double bb[9], double ir, int64_t box
     // every candidate radius is bounded by the global largest diameter;
     // arrivals and ghosts bring uids this context has not seen
     c->max_diam = std::max(c->max_diam, bb[6]);
+    c->min_diam = -INFINITY;   // arrivals and ghosts: diameters this context has not seen
     c->uid32 = false;
     planes[0] = S.x0;
     planes[1] = S.x1;
@@ -1656,8 +1709,7 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
     A.slots = c->slots;
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
     if (no > 0) {
-        if (fused) list_sweep_kernel<T, true><<<cdiv(no, kListThreads), kListThreads, 0, st>>>(A);
-        else list_sweep_kernel<T><<<cdiv(no, kListThreads), kListThreads, 0, st>>>(A);
+        launch_list_sweep<T>(c, A, no, fused, st);
         LAUNCH_CHECK(c);
         c->launches += 1;
     }
@@ -1850,14 +1902,15 @@ static int behavior_t(cg_context *c, int64_t step_index, double rate, double div
         c->uid32 = c->uid32 && last < (1ull << 32);
     }
     // new diameters (and daughters): the largest diameter and the bbox are recomputed
-    CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, sizeof(unsigned long long), st));
+    CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, 2 * sizeof(unsigned long long), st));
     max_diam_kernel<T><<<std::min(c->sms * 4, cdiv(c->n, kThreads)), kThreads, 0, st>>>((int)c->n, rec, c->maxd_enc);
     LAUNCH_CHECK(c);
     c->launches += 1;
-    unsigned long long enc = 0;
-    CUDA_TRY(c, cudaMemcpyAsync(&enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
+    unsigned long long enc[2] = {0, 0};
+    CUDA_TRY(c, cudaMemcpyAsync(enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));
-    c->max_diam = dec_ordered(enc);
+    c->max_diam = dec_ordered(enc[0]);
+    c->min_diam = c->n ? -dec_ordered(enc[1]) : -INFINITY;
     c->bbox_valid = false;
     c->list_valid = false;      // lists were built for the old radii
     c->last_kind = 0;
@@ -1919,7 +1972,7 @@ int cg_create(int device, int precision, cg_context **out)
     };
     chk(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     chk(cudaMalloc(&c->slots, sizeof(unsigned long long) * kSlots * kSlotWords));
-    chk(cudaMalloc(&c->maxd_enc, sizeof(unsigned long long)));
+    chk(cudaMalloc(&c->maxd_enc, 2 * sizeof(unsigned long long)));
     chk(cudaMalloc(&c->ovf_count, sizeof(unsigned)));
     chk(cudaMalloc(&c->block_counters, sizeof(unsigned long long) * 3 * kMaxCounterBlocks));
     chk(cudaMalloc(&c->bbox_dev, sizeof(double) * 16));
@@ -2076,7 +2129,7 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
                                                        (const float *)tmp4[2], (const float *)tmp4[3],
                                                        (Rec<float> *)c->b.rec[0]);
     for (int a = 0; a < 3; ++a) CUDA_TRY(c, cudaMemsetAsync(c->b.disp[a], 0, fe, st));
-    CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, sizeof(unsigned long long), st));
+    CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, 2 * sizeof(unsigned long long), st));
     if (!c->maxuid_dev) CUDA_TRY(c, cudaMalloc(&c->maxuid_dev, sizeof(unsigned long long)));
     CUDA_TRY(c, cudaMemsetAsync(c->maxuid_dev, 0, sizeof(unsigned long long), st));
     max_uid_kernel<<<std::min(c->sms * 4, nblk), kThreads, 0, st>>>((int)n, c->b.uid[0], c->maxuid_dev);
@@ -2088,11 +2141,12 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
             (int)n, (const Rec<float> *)c->b.rec[0], c->maxd_enc);
     LAUNCH_CHECK(c);
     c->launches += 3;
-    unsigned long long enc = 0, mu = 0;
-    CUDA_TRY(c, cudaMemcpyAsync(&enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
+    unsigned long long enc[2] = {0, 0}, mu = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(enc, c->maxd_enc, sizeof enc, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaMemcpyAsync(&mu, c->maxuid_dev, sizeof mu, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));   // host buffers are only borrowed
-    c->max_diam = dec_ordered(enc);
+    c->max_diam = dec_ordered(enc[0]);
+    c->min_diam = n ? -dec_ordered(enc[1]) : -INFINITY;
     c->uid32 = mu < (1ull << 32);
     return CG_OK;
 }
@@ -2353,6 +2407,7 @@ int cg_force_phase(cg_context *c, int64_t n, const void *px, const void *py, con
     // radii were uploaded in the diameter slot: double them (exact)
     if (c->prec == CG_FP64) double_diameter<double><<<nblk, kThreads, 0, st>>>(nn, (Rec<double> *)c->b.rec[0]);
     else double_diameter<float><<<nblk, kThreads, 0, st>>>(nn, (Rec<float> *)c->b.rec[0]);
+    c->min_diam = -INFINITY;
     long long *dbox = (long long *)c->b.stage;
     CUDA_TRY(c, cudaMemcpyAsync(dbox, box_index, sizeof(long long) * n, cudaMemcpyHostToDevice, st));
     keys_from_flat<<<nblk, kThreads, 0, st>>>(nn, dbox, c->count, c->b.key_rank);

@@ -181,15 +181,25 @@ __global__ void finish_step(unsigned long long *__restrict__ slots, double max_d
     }
 }
 
-// max(diameter) once per upload (the path never changes diameters)
+// max(diameter) and min(diameter) once per upload / behaviour phase (the
+// mechanical step never changes diameters): out[0] = enc(max), out[1] =
+// enc(-min).  A uniform pool (min == max) lets the list sweep take its pair
+// constants from the host.
 template <typename T>
 __global__ void max_diam_kernel(int n, const Rec<T> *__restrict__ rec, unsigned long long *__restrict__ out)
 {
-    double v = -INFINITY;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        v = fmax(v, (double)rec[i].d);
+    double v = -INFINITY, w = -INFINITY;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double d = (double)rec[i].d;
+        v = fmax(v, d);
+        w = fmax(w, -d);
+    }
     v = warp_max(v);
-    if ((threadIdx.x & 31) == 0 && v != -INFINITY) atomicMax(out, enc_ordered(v));
+    w = warp_max(w);
+    if ((threadIdx.x & 31) == 0 && v != -INFINITY) {
+        atomicMax(out, enc_ordered(v));
+        atomicMax(out + 1, enc_ordered(w));
+    }
 }
 
 // max(uid) once per upload: every uid below 2^32 lets the sweep take its

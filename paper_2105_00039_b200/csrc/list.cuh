@@ -45,6 +45,10 @@ struct ListArgs {
     double invL;              // FUSED: 1 / box length
     unsigned long long *slots;
     double shell_lo[3], shell_hi[3];
+    // UNI (every diameter equal): the pair constants, computed on the host in
+    // the pool dtype with the kernel's expressions -- rsum = ri + ri,
+    // req = (ri * ri) / rsum, bound = rsum * rsum * reject_factor
+    T u_rsum, u_req, u_bound;
 };
 
 template <typename T>
@@ -129,7 +133,11 @@ __device__ __forceinline__ float reject_factor<float>() { return 1.00000048f; }
 // whose operands leave the fast range, or with coincident centres, is redone
 // by list_agent_slow.  Entries are consumed in list (uid) order, so the sums
 // are the reference's.
-template <typename T, bool FUSED = false>
+//
+// UNI: a uniform pool -- rj, rsum, the rejection bound and req are kernel
+// constants (bitwise the values the per-pair expressions give), which frees
+// the registers of the per-partner cache and three FP64 operations per entry.
+template <typename T, bool FUSED = false, bool UNI = false>
 __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(ListArgs<T> A)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -198,15 +206,17 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
             if (p + 1 < cnt) o = A.rec[jn];
             if (p + 2 < cnt) jnn = __ldg(L + (p + 2) * A.nbr_stride);
             const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;
-            const T rj = co.d * half;
+            const T rj = UNI ? zero : co.d * half;
             const T s2 = dx * dx + dy * dy + dz * dz;
-            const T rsum = ri + rj;
-            if (s2 > rsum * rsum * kfac) continue;
+            const T rsum = UNI ? A.u_rsum : ri + rj;
+            if (s2 > (UNI ? A.u_bound : rsum * rsum * kfac)) continue;
             const T dist = tsqrt_nocall(s2, ok);
             const T delta = rsum - dist;
             if (!(delta > zero)) continue;
             ++nk;
-            if (rj != last_rj) {
+            if (UNI) {
+                last_req = A.u_req;
+            } else if (rj != last_rj) {
                 last_rj = rj;
                 last_req = tdiv_nocall(ri * rj, rsum, ok);
             }

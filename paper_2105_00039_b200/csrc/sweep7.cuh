@@ -78,6 +78,9 @@ struct Sweep7Args {
     int big_cap;                // power of two
     int *ovf2;                  // agents beyond big_cap: the thread-per-agent rounds
     unsigned *ovf2_count;
+    // UNI (every diameter equal, fp64): the pair constants in the kernel's
+    // expression order -- rsum = ri + ri, req = (ri * ri) / rsum, lim = rsum + skin
+    T u_rsum, u_req, u_lim;
 };
 
 constexpr int kListCap = 48;    // list width of sparse pools (dense pools: sized from the density)
@@ -129,8 +132,9 @@ __device__ __forceinline__ void f2_unpack(f32x2 v, float &lo, float &hi)
 // agent's neighbour list; the walk then covers the 5x5x5 box stencil (a
 // partner within ri + rmax + skin <= 2L can sit two boxes away), while m still
 // counts the reference's 27 boxes.
+// UNI: a uniform pool; rj, rsum, req and the list limit are kernel constants.
 template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, bool DEFER, bool LIST = false,
-          bool KEY32 = false>
+          bool KEY32 = false, bool UNI = false>
 __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s, unsigned &c_m,
                                             unsigned &c_nk, unsigned &c_nd, float &dmax2)
 {
@@ -280,17 +284,19 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                     o = A.rec[j];
                 }
                 const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;   // kernels.py:198-203
-                const T rj = co.d * half;
+                const T rj = UNI ? zero : co.d * half;
                 const T dist = xsqrt(dx * dx + dy * dy + dz * dz);
-                const T rsum = ri + rj;
-                if (LIST && dist <= rsum + A.skin) {
+                const T rsum = UNI ? A.u_rsum : ri + rj;
+                if (LIST && dist <= (UNI ? A.u_lim : rsum + A.skin)) {
                     if (nl < A.list_cap) A.nbr[nl * A.nbr_stride + a] = jc;
                     ++nl;
                 }
                 const T delta = rsum - dist;
                 if (!(delta > zero)) continue;
                 ++nk;                                                    // kernels.py:230-257
-                if (rj != last_rj) {
+                if (UNI) {
+                    last_req = A.u_req;
+                } else if (rj != last_rj) {
                     last_rj = rj;
                     last_req = xdiv(ri * rj, rsum);
                 }
@@ -495,13 +501,14 @@ __device__ __forceinline__ void warp_dmax(unsigned long long *slots, float dmax2
         atomicMax(slots + (blockIdx.x % kSlots) * kSlotWords + 9, enc_ordered((double)dmax2));
 }
 
-template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, int MINB, bool LIST = false, bool KEY32 = false>
+template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, int MINB, bool LIST = false, bool KEY32 = false,
+          bool UNI = false>
 __global__ void __launch_bounds__(kThreads, MINB) sweep7_kernel(Sweep7Args<T> A)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
     float dmax2 = 0.f;
-    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true, LIST, KEY32>(A, s, c_m, c_nk, c_nd, dmax2);
+    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true, LIST, KEY32, UNI>(A, s, c_m, c_nk, c_nd, dmax2);
     warp_counters(A.slots, c_m, c_nk, c_nd);
     if (LIST || ZSORTED) warp_dmax(A.slots, dmax2);
 }
