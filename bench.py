@@ -309,7 +309,7 @@ def main_slab(args, rank, world, local):
     ctx.set_option(_native.CG_OPT_SUMMATION, {"uid": 0, "stencil": 1}[args.summation])
     ctx.reserve(int(n0 * 1.05) + 4 * 256 * 256 * 2 + 4096)
     ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
-    ex = TorchExchange(device="cuda", device_buffers=args.exchange == "nccl")
+    ex = TorchExchange(device="cuda", device_buffers=args.exchange == "nccl", stream=ctx.stream)
     # counters all-reduced once for the timed steps (inside the timed region)
     runner = SlabRunner(ctx, ex, sync_counters=False)
     params = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
@@ -337,11 +337,15 @@ def main_slab(args, rank, world, local):
     total = stats[-1].agents
     value = total / (ms * 1e-3)
     # the dominant sweep kernel over the timed steps still in the stats ring
-    kinds = {}
+    kinds, totals = {}, {}
     for k in range(min(args.steps, 60)):
         s_ = ctx.fetch_stats(ctx.steps - 1 - k)
         kinds.setdefault(int(s_.sweep_kind), []).append(float(s_.t_force_ms))
+        totals.setdefault(int(s_.sweep_kind), []).append(float(s_.t_total_ms))
     dom = max(kinds, key=lambda k: sum(kinds[k]))
+    names = {0: "grid_sweep", 1: "grid_sweep_list_build", 2: "list_sweep"}
+    sweep_mix = {names[k]: {"steps": len(v), "mean_ms": float(np.mean(v)), "mean_step_device_ms": float(np.mean(totals[k]))}
+                 for k, v in sorted(kinds.items())}
     t_force = reduce_max(float(np.mean(kinds[dom])), world)
     kernel_name = {0: "sweep7_kernel", 1: "sweep7_kernel_list_build", 2: "list_sweep_kernel"}[dom]
     n_local = ctx.n
@@ -395,7 +399,8 @@ def main_slab(args, rank, world, local):
                                   "neighbour-list steps" % (world, args.exchange)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": kernel_name + " (per GPU)",
-                     "alg_bytes_per_agent": bal, "kernel_ms": t_force, "peak_source": peak_src},
+                     "alg_bytes_per_agent": bal, "kernel_ms": t_force, "peak_source": peak_src,
+                     "sweep_mix": sweep_mix},
         "step_roofline_frac": total / world * bal / (ms * 1e-3) / 1e9 / peak,
         "pair_interactions_per_s": stats[-1].force_evals / (ms * 1e-3),
         "candidates_per_s": stats[-1].candidates / (ms * 1e-3),

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CG_ABI_VERSION 5
+#define CG_ABI_VERSION 6
 
 /* status codes */
 #define CG_OK 0
@@ -161,7 +161,7 @@ int cg_unit_vectors(cg_context *ctx, int64_t n, const uint64_t *uid, int64_t ste
 /* Neighbour-list reuse counters (CG_OPT_LIST_SKIN): out[0] list builds,
  * out[1] steps served from lists, out[2] lists currently valid, out[3] skin of
  * the last build in 1e-6 length units. */
-int cg_list_stats(cg_context *ctx, int64_t out[4]);
+int cg_list_stats(cg_context *ctx, int64_t out[5]);
 
 /* ---- radius queries: kernels.grid_neighbor_counts /
  * grid_neighbor_fill (kernels.py:427-520) behind spatial.neighbor_counts /
@@ -181,19 +181,24 @@ int cg_neighbor_fill(cg_context *ctx, double radius, const int64_t *indptr, int6
  * X_r+1 as ghosts.  Device buffers (send/recv) are raw device pointers owned
  * by the caller (e.g. torch CUDA tensors handed to NCCL); records are
  * cg_record_bytes() each.  Per step, on every rank, ONE exchange round:
- *   cg_local_bbox -> all-reduce (min/min/min/max/max/max/max) -> cg_slab_plan
- *   -> all-to-all of the 3-per-rank counts -> cg_slab_pack(send) ->
- *   all-to-all of the records -> cg_slab_unpack(recv) -> cg_slab_step.
+ *   cg_local_bbox -> all-reduce (MAX of the 11 values, minima negated) ->
+ *   cg_slab_plan -> all-to-all of the 3-per-rank counts -> cg_slab_pack(send)
+ *   -> exchange of the records -> cg_slab_unpack(recv) -> cg_slab_step.
+ * pack, unpack and step are enqueued on the context's stream (cg_stream) and
+ * do not wait for the host: the caller orders its exchange of send / recv on
+ * that stream (or waits on it), as NCCL does when issued on cg_stream.
  * Owned agents' results are those of a single-GPU step over the global pool. */
 int64_t cg_record_bytes(const cg_context *ctx);
 /* Pre-size the agent buffers (before cg_upload) for arrivals and ghosts. */
 int cg_reserve(cg_context *ctx, int64_t capacity);
 /* Exact bbox of the owned agents (min xyz, max xyz), max diameter, the last
- * step's largest squared displacement, and a neighbour-list veto (the build's
+ * step's largest squared displacement, a neighbour-list veto (the build's
  * overflow count, or 1 when this rank neither built lists nor ran a list step
- * last): all nine are all-reduced with MAX (after negating the three minima),
- * so every rank takes the same list decision in cg_slab_plan. */
-int cg_local_bbox(cg_context *ctx, double out[9]);
+ * last), the negated min diameter and the largest uid: all eleven are
+ * all-reduced with MAX (after negating the three minima), so every rank takes
+ * the same list decision in cg_slab_plan and knows whether the global pool is
+ * uniform and whether every uid is below 2^32. */
+int cg_local_bbox(cg_context *ctx, double out[11]);
 /* Geometry from the global bbox (spatial.py:99-116; GridOverflowError as
  * cg_step) and slab planes: planes = {X_rank, X_rank+1}.  counts (3 * world):
  * for destination rank q, counts[3q] = owned agents that migrate to q (0 for
@@ -203,7 +208,7 @@ int cg_local_bbox(cg_context *ctx, double out[9]);
  * valid (decided identically on every rank from the all-reduced bbox[7..8])
  * keeps the partition: no migrants, and the ghost runs are the refresh of the
  * ghosts every rank holds since the last rebuild. */
-int cg_slab_plan(cg_context *ctx, const double bbox[9], double interaction_radius, int64_t box_cap,
+int cg_slab_plan(cg_context *ctx, const double bbox[11], double interaction_radius, int64_t box_cap,
                  int world, int rank, int64_t *counts, int64_t planes[2]);
 /* Outgoing records -> send, grouped by destination rank (ascending), each
  * destination's run = [migrants][lo ghosts][hi ghosts] with the cg_slab_plan
@@ -215,6 +220,12 @@ int cg_slab_pack(cg_context *ctx, void *send);
 int cg_slab_unpack(cg_context *ctx, const void *recv, const int64_t *recv_counts);
 /* The mechanical step on the owned agents over the slab's sub-grid. */
 int cg_slab_step(cg_context *ctx, const double params[5], int flags, cg_step_stats *stats);
+/* Optional, between cg_slab_pack and cg_slab_unpack of a neighbour-list step:
+ * enqueue the list sweep of the owned agents whose lists hold no ghost (build
+ * planes at least 3 from either slab face) so it runs while the ghost refresh
+ * is in flight; the following cg_slab_step sweeps only the boundary agents.
+ * A no-op on rebuild steps (same flags as the cg_slab_step that follows). */
+int cg_slab_step_interior(cg_context *ctx, const double params[5], int flags);
 /* After cg_slab_plan: -1 for a rebuild step, else the id of the list epoch
  * (constant between rebuilds): a refresh step whose run sizes -- sent and
  * received -- are those of the previous refresh step of the same epoch, so a

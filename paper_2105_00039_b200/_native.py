@@ -30,7 +30,7 @@ EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_
             "cg_record_export", "cg_box_ids", "cg_force_phase", "cg_launch_count",
             "cg_host_alloc", "cg_host_free", "cg_record_bytes", "cg_reserve", "cg_local_bbox",
             "cg_slab_plan", "cg_slab_pack", "cg_slab_unpack",
-            "cg_slab_step", "cg_neighbor_counts", "cg_neighbor_fill",
+            "cg_slab_step", "cg_slab_step_interior", "cg_neighbor_counts", "cg_neighbor_fill",
             "cg_list_stats", "cg_slab_list_epoch", "cg_step_download", "cg_behavior",
             "cg_unit_vectors")
 
@@ -116,12 +116,13 @@ def load():
         "cg_slab_pack": ([_P, _P], ctypes.c_int),
         "cg_slab_unpack": ([_P, _P, _P], ctypes.c_int),
         "cg_slab_step": ([_P, _P, ctypes.c_int, ctypes.POINTER(StepStatsC)], ctypes.c_int),
+        "cg_slab_step_interior": ([_P, _P, ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
-    if L.cg_abi_version() != 5:
+    if L.cg_abi_version() != 6:
         raise NativeUnavailable("ABI version mismatch")
     _lib = L
     return L
@@ -277,11 +278,12 @@ class Context:
         return out
 
     def list_stats(self):
-        """(builds, list steps, valid, skin) of the neighbour-list reuse."""
-        out = np.zeros(4, np.int64)
+        """(builds, list steps, valid, skin, slab list steps with the interior
+        sweep overlapping the ghost refresh) of the neighbour-list reuse."""
+        out = np.zeros(5, np.int64)
         check(load().cg_list_stats(self.h, ptr(out)), self.h)
         return {"builds": int(out[0]), "list_steps": int(out[1]), "valid": bool(out[2]),
-                "skin": out[3] * 1e-6}
+                "skin": out[3] * 1e-6, "overlapped": int(out[4])}
 
     # ---- radius queries (spatial.neighbor_counts / neighbor_csr)
     def neighbor_counts(self, radius):
@@ -307,8 +309,9 @@ class Context:
 
     def local_bbox(self):
         """min xyz, max xyz, max diameter, last step's largest squared
-        displacement, last step's neighbour-list overflows (cg_local_bbox)."""
-        out = np.empty(9, np.float64)
+        displacement, last step's neighbour-list overflows, -min diameter,
+        max uid (cg_local_bbox)."""
+        out = np.empty(11, np.float64)
         check(load().cg_local_bbox(self.h, ptr(out)), self.h)
         return out
 
@@ -334,6 +337,12 @@ class Context:
         rc = np.ascontiguousarray(recv_counts, np.int64)
         check(load().cg_slab_unpack(self.h, recv_ptr, ptr(rc)), self.h)
         self.n = int(load().cg_count(self.h))
+
+    def slab_step_interior(self, params5, flags=0):
+        """cg_slab_step_interior: the interior rows' list sweep, enqueued before
+        the ghost refresh is unpacked (a no-op on rebuild steps)."""
+        p = np.ascontiguousarray(params5, np.float64)
+        check(load().cg_slab_step_interior(self.h, ptr(p), int(flags)), self.h)
 
     def slab_step(self, params5, flags=0, wait=True):
         p = np.ascontiguousarray(params5, np.float64)

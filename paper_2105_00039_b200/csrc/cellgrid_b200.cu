@@ -156,7 +156,9 @@ struct cg_context {
     double list_skin_used = 0.0;
     int list_life = 0, list_backoff = 0, list_wait = 0;
     int64_t list_builds = 0, list_steps = 0;
-    bool uid32 = false;           // every stored uid < 2^32 (set at upload; slab exchanges clear it)
+    int64_t overlapped_steps = 0;   // slab list steps whose interior sweep ran before the ghost refresh
+    bool uid32 = false;           // every stored uid < 2^32 (upload, behaviour phase; slabs: the global max uid)
+    uint64_t max_uid = 0;         // largest stored uid (upload, behaviour phase)
     void *beh = nullptr;          // behaviour phase scratch (ripe list, sort buffers), beh_bytes
     size_t beh_bytes = 0;
     unsigned long long *maxuid_dev = nullptr;
@@ -192,6 +194,12 @@ struct cg_context {
         bool unpacked = false;
         int64_t n_total = 0;       // owned + ghosts kept between rebuilds
         int rot_build = 0;         // index of the first owned agent (the lo-ghost count)
+        // list steps: owned rows [rot_build + b_lo, rot_build + n_owned - b_hi)
+        // hold no ghost in their lists (build planes >= 3 from either slab face)
+        // and may be swept before the ghost refresh lands (cg_slab_step_interior)
+        bool split_ok = false;
+        int b_lo = 0, b_hi = 0;
+        bool interior_done = false;
         double x_lo_abs = 0, x_hi_abs = 0;   // the owned slab's x range at the rebuild
         int64_t ref_counts[kHist] = {};      // refresh records per (destination, kind)
         int64_t ref_total = 0;
@@ -1013,6 +1021,7 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
     CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
     ListArgs<T> A{};
+    A.skip_at = INT_MAX;
     A.n = n;
     A.g = g;
     A.bd = c->bd;
@@ -1384,7 +1393,7 @@ static SlabCols<T> cur_cols(cg_context *c)
 }
 
 template <typename T>
-static int slab_plan_t(cg_context *c, const double bb[9], double ir, int64_t box_cap, int world, int rank,
+static int slab_plan_t(cg_context *c, const double bb[11], double ir, int64_t box_cap, int world, int rank,
                        int64_t *counts, int64_t planes[2])
 {
     auto &S = c->slab;
@@ -1402,6 +1411,10 @@ static int slab_plan_t(cg_context *c, const double bb[9], double ir, int64_t box
     if (lists_on) slab_list_account<T>(c, bb);
     S.list_mode = lists_on && c->list_valid && S.refresh_ready && c->nbr_cap == c->cap &&
                   2.0 * c->list_D <= 0.999 * c->list_skin_used;
+    // the global diameter range: every agent a rank holds (owned, arrived or a
+    // ghost) lies in it, so min == max is a uniform pool everywhere
+    c->max_diam = std::max(c->max_diam, bb[6]);
+    c->min_diam = std::isfinite(bb[9]) ? -bb[9] : -INFINITY;
     S.unpacked = false;
     S.g = g;
     if (S.list_mode) {
@@ -1411,6 +1424,7 @@ static int slab_plan_t(cg_context *c, const double bb[9], double ir, int64_t box
         planes[1] = S.x1;
         S.planned = true;
         S.packed = false;
+        S.interior_done = false;
         return CG_OK;
     }
     if (c->list_valid && lists_on) {   // expired lists: the same backoff rule as a single context
@@ -1442,9 +1456,8 @@ static int slab_plan_t(cg_context *c, const double bb[9], double ir, int64_t box
     }
     // every candidate radius is bounded by the global largest diameter;
     // arrivals and ghosts bring uids this context has not seen
-    c->max_diam = std::max(c->max_diam, bb[6]);
-    c->min_diam = -INFINITY;   // arrivals and ghosts: diameters this context has not seen
-    c->uid32 = false;
+    // arrivals and ghosts bring uids this context has not seen: the global max
+    c->uid32 = bb[10] < 4294967296.0;
     planes[0] = S.x0;
     planes[1] = S.x1;
     cudaStream_t st = c->stream;
@@ -1464,6 +1477,7 @@ static int slab_plan_t(cg_context *c, const double bb[9], double ir, int64_t box
     for (int k = 0; k < 3 * world; ++k) counts[k] = S.h_counts[k];
     S.planned = true;
     S.packed = false;
+    S.interior_done = false;
     return CG_OK;
 }
 
@@ -1479,8 +1493,7 @@ static int slab_pack_t(cg_context *c, void *send)
             LAUNCH_CHECK(c);
             c->launches += 1;
         }
-        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-        return CG_OK;
+        return CG_OK;   // the exchange is ordered after the pack on the context stream
     }
     const int n = (int)c->n_owned;
     const int W = S.world;
@@ -1509,8 +1522,7 @@ static int slab_pack_t(cg_context *c, void *send)
         slab_fill_holes<T><<<cdiv(hc[1], kThreads), kThreads, 0, st>>>((int)hc[1], S.holes, S.movers, C);
     LAUNCH_CHECK(c);
     c->launches += 3;
-    CUDA_TRY(c, cudaStreamSynchronize(st));   // the send buffer is handed to the exchange
-    c->n = c->n_owned = n_keep;
+    c->n = c->n_owned = n_keep;   // the exchange is ordered after the pack on the context stream
     c->bbox_valid = false;
     return CG_OK;
 }
@@ -1635,56 +1647,67 @@ static int slab_list_tables(cg_context *c)
     S.x_lo_abs = S.g.ox + (double)S.x0 * S.g.L;
     S.x_hi_abs = S.g.ox + (double)S.x1 * S.g.L;
     S.refresh_ready = true;
+    // interior rows: with relaid storage the owned rows are the build's slots
+    // in plane order, so the boundary rows (build planes within 3 of a slab
+    // face -- list partners are within ri + rj + skin <= 2L) are the two ends
+    S.split_ok = false;
+    S.b_lo = no;
+    S.b_hi = 0;
+    const Geometry &gb = c->geo;
+    if (c->relaid && no > 0 && S.x1 - S.x0 >= 7 && gb.xoff <= S.x0) {
+        const int64_t P = (int64_t)gb.dimy * gb.dimz;
+        const int64_t at[4] = {(S.x0 - gb.xoff) * P, (S.x0 + 3 - gb.xoff) * P, (S.x1 - 3 - gb.xoff) * P,
+                               (S.x1 - gb.xoff) * P};
+        int h[4];
+        for (int k = 0; k < 4; ++k)
+            CUDA_TRY(c, cudaMemcpyAsync(h + k, c->offset + at[k], sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        if (h[0] == lo && h[3] == lo + no && h[0] <= h[1] && h[1] <= h[2] && h[2] <= h[3]) {
+            S.b_lo = h[1] - h[0];
+            S.b_hi = h[3] - h[2];
+            S.split_ok = true;
+        }
+    }
     return CG_OK;
 }
 
 // a list step on a slab: grid counts over owned + ghosts, list sweep of the
-// owned agents (indices [rot, rot + n_owned), buffers at index - rot)
+// owned agents (indices [rot, rot + n_owned), buffers at index - rot).
+// part 1 (cg_slab_step_interior, before the ghost refresh is unpacked): set-up
+// and the sweep of the interior rows; part 2 (cg_slab_step): the rest -- all
+// rows, or only the boundary rows when part 1 ran.
 template <typename T>
-static int slab_list_step(cg_context *c, const double params[5], bool freeze, bool record)
+static int slab_list_step(cg_context *c, const double params[5], bool freeze, bool record, int part)
 {
     auto &S = c->slab;
     const int slot = (int)(c->steps_done % kRing);
     cudaStream_t st = c->stream;
     const int rot = S.rot_build, nt = (int)S.n_total, no = (int)c->n_owned;
-    // sub-grid: every present agent lies within 3 box lengths (+ the motion
-    // since the rebuild) of the owned slab's x range at the rebuild
-    Geometry g = S.g;
-    const auto plane = [&](double x) {
-        return (int)std::min<double>(std::max<double>(std::floor((x - S.g.ox) / S.g.L), 0.0), S.g.dimx - 1.0);
-    };
-    const int xl = plane(S.x_lo_abs - 4.0 * S.g.L), xh = plane(S.x_hi_abs + 4.0 * S.g.L) + 1;
-    g.xoff = xl;
-    g.gdimx = S.g.dimx;
-    g.dimx = std::max(xh - xl, 1);
-    g.nb = g.dimx * g.dimy * g.dimz;
-    CUDA_TRY(c, cudaEventRecord(c->ev[slot][0], st));
-    int rc;
-    if ((rc = ensure_boxes(c, g.nb))) return rc;
-    c->geo = g;
-    c->bd = make_decode(g);
-    unsigned long long *stat = c->stat_dev + slot * kStatSlots;
-    CUDA_TRY(c, cudaMemsetAsync(stat, 0, sizeof(unsigned long long) * kStatSlots, st));
-    const int cp = c->cur_pos, ca = c->cur_attr;
     const bool fused = !record;   // box counting inside the list sweep (owned) + count_ghosts
-    if (!fused) {
-        box_keys<T><<<cdiv(nt, kThreads), kThreads, 0, st>>>(nt, g, 1.0 / g.L, (const Rec<T> *)c->b.rec[cp] - rot,
-                                                             c->count, c->b.key_rank);
-        LAUNCH_CHECK(c);
-        c->launches += 1;
-        if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
-    } else if (nt > no) {
-        count_ghosts<T><<<cdiv(nt - no, kThreads), kThreads, 0, st>>>(nt, rot, no, g, 1.0 / g.L,
-                                                                       (const Rec<T> *)c->b.rec[cp] - rot, c->count,
-                                                                       c->count_own);
-        LAUNCH_CHECK(c);
-        c->launches += 1;
+    int rc;
+    if (part == 1 || !S.interior_done) {
+        // sub-grid: every present agent lies within 3 box lengths (+ the motion
+        // since the rebuild) of the owned slab's x range at the rebuild
+        Geometry g = S.g;
+        const auto plane = [&](double x) {
+            return (int)std::min<double>(std::max<double>(std::floor((x - S.g.ox) / S.g.L), 0.0), S.g.dimx - 1.0);
+        };
+        const int xl = plane(S.x_lo_abs - 4.0 * S.g.L), xh = plane(S.x_hi_abs + 4.0 * S.g.L) + 1;
+        g.xoff = xl;
+        g.gdimx = S.g.dimx;
+        g.dimx = std::max(xh - xl, 1);
+        g.nb = g.dimx * g.dimy * g.dimz;
+        CUDA_TRY(c, cudaEventRecord(c->ev[slot][0], st));
+        if ((rc = ensure_boxes(c, g.nb))) return rc;
+        c->geo = g;
+        c->bd = make_decode(g);
+        CUDA_TRY(c, cudaMemsetAsync(c->stat_dev + slot * kStatSlots, 0, sizeof(unsigned long long) * kStatSlots, st));
     }
-    CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
-    CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
+    const Geometry g = c->geo;
+    unsigned long long *stat = c->stat_dev + slot * kStatSlots;
+    const int cp = c->cur_pos, ca = c->cur_attr;
     ListArgs<T> A{};
-    A.n = no;
-    A.own_lo = rot;
+    A.skip_at = INT_MAX;
     A.g = g;
     A.bd = c->bd;
     A.key_rank = c->b.key_rank;
@@ -1708,8 +1731,43 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
     A.invL = 1.0 / g.L;
     A.slots = c->slots;
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
-    if (no > 0) {
-        launch_list_sweep<T>(c, A, no, fused, st);
+    const int n_int = no - S.b_lo - S.b_hi;
+    if (part == 1) {   // interior rows: their lists hold no ghost
+        if (n_int > 0) {
+            A.n = n_int;
+            A.own_lo = rot + S.b_lo;
+            launch_list_sweep<T>(c, A, n_int, true, st);
+            LAUNCH_CHECK(c);
+            c->launches += 1;
+        }
+        S.interior_done = true;
+        c->overlapped_steps++;
+        return CG_OK;
+    }
+    if (!fused) {
+        box_keys<T><<<cdiv(nt, kThreads), kThreads, 0, st>>>(nt, g, 1.0 / g.L, (const Rec<T> *)c->b.rec[cp] - rot,
+                                                             c->count, c->b.key_rank);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        if ((rc = launch_scan_rts(c, g.nb, stat))) return rc;
+    } else if (nt > no) {
+        count_ghosts<T><<<cdiv(nt - no, kThreads), kThreads, 0, st>>>(nt, rot, no, g, 1.0 / g.L,
+                                                                       (const Rec<T> *)c->b.rec[cp] - rot, c->count,
+                                                                       c->count_own);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][1], st));
+    CUDA_TRY(c, cudaEventRecord(c->ev[slot][2], st));
+    A.own_lo = rot;
+    A.n = no;
+    if (S.interior_done) {   // the boundary rows: [0, b_lo) and [no - b_hi, no)
+        A.n = S.b_lo + S.b_hi;
+        A.skip_at = S.b_lo;
+        A.skip = n_int;
+    }
+    if (A.n > 0) {
+        launch_list_sweep<T>(c, A, A.n, fused, st);
         LAUNCH_CHECK(c);
         c->launches += 1;
     }
@@ -1750,7 +1808,8 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
     const bool freeze = (flags & CG_STEP_FREEZE) != 0;
     const bool record = (flags & CG_STEP_RECORD) != 0;
     if (S.list_mode) {
-        if ((rc = slab_list_step<T>(c, params, freeze, record))) return rc;
+        if ((rc = slab_list_step<T>(c, params, freeze, record, 2))) return rc;
+        S.interior_done = false;
         if (!freeze) c->cur_pos = 1 - c->cur_pos;
         c->last_kind = 2;
         St.sweep_kind = 2;
@@ -1900,6 +1959,7 @@ static int behavior_t(cg_context *c, int64_t step_index, double rate, double div
         c->n = c->n_owned = n + k;
         const uint64_t last = next_uid + k - 1;
         c->uid32 = c->uid32 && last < (1ull << 32);
+        c->max_uid = std::max<uint64_t>(c->max_uid, last);
     }
     // new diameters (and daughters): the largest diameter and the bbox are recomputed
     CUDA_TRY(c, cudaMemsetAsync(c->maxd_enc, 0, 2 * sizeof(unsigned long long), st));
@@ -2148,6 +2208,7 @@ int cg_upload(cg_context *c, int64_t n, const void *px, const void *py, const vo
     c->max_diam = dec_ordered(enc[0]);
     c->min_diam = n ? -dec_ordered(enc[1]) : -INFINITY;
     c->uid32 = mu < (1ull << 32);
+    c->max_uid = mu;
     return CG_OK;
 }
 
@@ -2469,7 +2530,7 @@ int cg_reserve(cg_context *c, int64_t capacity)
     return CG_OK;
 }
 
-int cg_local_bbox(cg_context *c, double out[9])
+int cg_local_bbox(cg_context *c, double out[11])
 {
     if (!c) return CG_ERR_VALUE;
     CUDA_TRY(c, cudaSetDevice(c->device));
@@ -2479,6 +2540,8 @@ int cg_local_bbox(cg_context *c, double out[9])
         out[6] = c->max_diam;
         out[7] = 0.0;
         out[8] = c->last_kind == 2 ? 0.0 : 1.0;   // no lists of its own: veto list steps
+        out[9] = -INFINITY;                       // no diameters of its own
+        out[10] = 0.0;
         return CG_OK;
     }
     int rc = CG_OK;
@@ -2500,10 +2563,16 @@ int cg_local_bbox(cg_context *c, double out[9])
     // list veto: overflows of a build, or 1 when this rank neither built lists
     // nor ran a list step last (every rank must take the same decision)
     out[8] = c->last_kind == 1 ? c->bbox_host[8] : (c->last_kind == 2 ? 0.0 : 1.0);
+    // -min diameter of the owned agents: the slab's own minimum until ghosts
+    // or arrivals widened the range (min_diam is then the global one)
+    out[9] = std::isfinite(c->min_diam) ? -c->min_diam : -INFINITY;
+    // the largest uid (all-reduced: 32-bit survivor sort keys when every uid
+    // of the global pool is below 2^32); rounded up to a double
+    out[10] = c->max_uid < (1ull << 53) ? (double)c->max_uid : 1.8446744073709552e19;
     return CG_OK;
 }
 
-int cg_slab_plan(cg_context *c, const double bbox[9], double interaction_radius, int64_t box_cap, int world,
+int cg_slab_plan(cg_context *c, const double bbox[11], double interaction_radius, int64_t box_cap, int world,
                  int rank, int64_t *counts, int64_t planes[2])
 {
     if (!c) return CG_ERR_VALUE;
@@ -2530,6 +2599,20 @@ int cg_slab_unpack(cg_context *c, const void *recv, const int64_t *recv_counts)
     if (c->slab.unpacked) return fail(c, CG_ERR_STATE, "cg_slab_unpack called twice");
     return c->prec == CG_FP64 ? slab_unpack_t<double>(c, recv, recv_counts)
                               : slab_unpack_t<float>(c, recv, recv_counts);
+}
+
+int cg_slab_step_interior(cg_context *c, const double params[5], int flags)
+{
+    if (!c) return CG_ERR_VALUE;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    auto &S = c->slab;
+    if (!S.planned || !S.packed || S.unpacked)
+        return fail(c, CG_ERR_STATE, "cg_slab_step_interior belongs between cg_slab_pack and cg_slab_unpack");
+    // nothing to overlap: a rebuild step, no interior, a recorded step, or twice
+    if (!S.list_mode || !S.split_ok || (flags & CG_STEP_RECORD) || S.interior_done) return CG_OK;
+    const bool freeze = (flags & CG_STEP_FREEZE) != 0;
+    return c->prec == CG_FP64 ? slab_list_step<double>(c, params, freeze, false, 1)
+                              : slab_list_step<float>(c, params, freeze, false, 1);
 }
 
 int cg_slab_step(cg_context *c, const double params[5], int flags, cg_step_stats *stats)
@@ -2652,13 +2735,14 @@ int cg_unit_vectors(cg_context *c, int64_t n, const uint64_t *uid, int64_t step,
     return CG_OK;
 }
 
-int cg_list_stats(cg_context *c, int64_t out[4])
+int cg_list_stats(cg_context *c, int64_t out[5])
 {
     if (!c || !out) return CG_ERR_VALUE;
     out[0] = c->list_builds;
     out[1] = c->list_steps;
     out[2] = c->list_valid ? 1 : 0;
     out[3] = (int64_t)llround(c->list_skin_used * 1e6);
+    out[4] = c->overlapped_steps;
     return CG_OK;
 }
 

@@ -36,6 +36,9 @@ struct ListArgs {
     const int *nbr;           // [list width][nbr_stride]
     const int *nbr_n;
     long long nbr_stride;
+    // rows swept: own_lo + t for t < skip_at, own_lo + t + skip beyond (a slab's
+    // boundary rows around the interior range swept earlier); no skip by default
+    int skip_at, skip;
     T *disp_x, *disp_y, *disp_z;
     Rec<T> *new_rec;          // nullptr when frozen
     int *rec_m, *rec_nk;      // nullptr unless recording
@@ -147,9 +150,10 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
         const int lane = threadIdx.x & 31;
         int flat = -1 - lane;   // distinct dummy keys past n
         if (t < A.n) {
-            const Rec<T> r = A.rec[A.own_lo + t];
+            const int row = A.own_lo + (t < A.skip_at ? t : t + A.skip);
+            const Rec<T> r = A.rec[row];
             flat = flat_box_fast(A.g, A.invL, r.x, r.y, r.z);
-            if (A.pkey) A.pkey[A.own_lo + t] = flat;
+            if (A.pkey) A.pkey[row] = flat;
         }
         const int prev = __shfl_up_sync(0xffffffffu, flat, 1);
         const bool start = lane == 0 || prev != flat;
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
         if (start && t < A.n) atomicAdd(A.count + flat, run_end - lane);
     }
     if (t < A.n) {
-        const int a = A.own_lo + t;
+        const int a = A.own_lo + (t < A.skip_at ? t : t + A.skip);
         int m = -1;
         if (!FUSED) {
         const int key = A.key_rank[a].x;

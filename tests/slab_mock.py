@@ -44,9 +44,12 @@ class MockSlabContext:
 
     def local_bbox(self):
         if self.n == 0:
-            return np.array([np.inf] * 3 + [-np.inf] * 3 + [float(self.cols["diameter"].max(initial=0.0)), 0, 0])
+            return np.array([np.inf] * 3 + [-np.inf] * 3 + [float(self.cols["diameter"].max(initial=0.0)), 0, 0,
+                                                            -np.inf, 0.0])
         p = [self.cols[c].astype(np.float64) for c in COLS[:3]]
-        return np.array([q.min() for q in p] + [q.max() for q in p] + [float(self.cols["diameter"].max()), 0, 0])
+        d = self.cols["diameter"].astype(np.float64)
+        return np.array([q.min() for q in p] + [q.max() for q in p] +
+                        [float(d.max()), 0, 0, -float(d.min()), float(self.uid.max())])
 
     def _ix(self, x):
         return np.clip(np.floor((x.astype(np.float64) - self.origin[0]) / self.L).astype(np.int64), 0,

@@ -39,7 +39,7 @@ def test_abi_version_and_no_device_behaviour():
     """Without a GPU every device entry point fails loudly (no CPU fallback)."""
     from paper_2105_00039_b200 import _native
     lib = _native.load()
-    assert lib.cg_abi_version() == 5
+    assert lib.cg_abi_version() == 6
     n = ctypes.c_int(-1)
     rc = lib.cg_device_count(ctypes.byref(n))
     try:

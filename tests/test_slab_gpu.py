@@ -117,3 +117,5 @@ def test_slab_ranks_match_single_context(cuda_required, world, summation, skin, 
     assert all(r[2][0][4] > 0 for r in res)          # ghosts were exchanged
     if skin != 0:                                    # list steps ran on every rank
         assert all(r[3]["list_steps"] > 0 and r[3]["builds"] > 0 for r in res), [r[3] for r in res]
+        if world <= 3 and not dense:                 # slabs of >= 7 planes: interior sweep before the refresh
+            assert all(r[3]["overlapped"] > 0 for r in res), [r[3] for r in res]

@@ -30,7 +30,7 @@ def main():
     ctx.set_option(_native.CG_OPT_SUMMATION, 1)
     ctx.reserve(int(pool.count * 1.05) + 4 * 256 * 256 * 2 + 4096)
     ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
-    ex = TorchExchange(device="cuda")
+    ex = TorchExchange(device="cuda", stream=ctx.stream)
     R = ctx.record_bytes
     params = np.array([2.0, 1.0, 0.01, 3.0, 1.0])
     stream = torch.cuda.ExternalStream(ctx.stream)
