@@ -177,14 +177,15 @@ def measured_hbm_peak():
         return 6650.0, "fallback"
 
 
-def profiled_traffic(config, precision, kernel):
-    """Per-launch DRAM bytes (read + write) of ``kernel`` from the committed
-    ncu --set full capture (profiles/traffic.json), if any."""
+def profiled_kernel(config, precision, kernel):
+    """ncu --set full figures of ``kernel`` from the committed capture
+    (profiles/kernel_metrics.json, written by tools/kernel_metrics.py): DRAM
+    bytes read + written per launch and the FP64 pipe's busy fraction."""
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get("%s_%s" % (config, precision), {}).get(kernel)
+        with open(os.path.join(ROOT, "profiles", "kernel_metrics.json")) as fh:
+            return json.load(fh).get("%s_%s" % (config, precision), {}).get(kernel) or {}
     except (OSError, ValueError, AttributeError):
-        return None
+        return {}
 
 
 def fp64_view(cands, evals, ms):
@@ -618,6 +619,7 @@ def main():
     peak, peak_src = measured_hbm_peak()
     bal = B_ALG[args.precision]
     achieved = n * bal / (t_force * 1e-3) / 1e9
+    prof = profiled_kernel(args.config, args.precision, kernel_name)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -627,7 +629,8 @@ def main():
                    "l2": "inputs larger than L2 (%.0f MB of agent state per GPU)" % (n * (6 * np.dtype(pool.dtype).itemsize + 8) / 1e6),
                    "parallelism": "single GPU" if world == 1 else "replicas x%d (no halo exchange)" % world},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.precision, kernel_name),
+                     "frac": achieved / peak, "traffic": prof.get("traffic"),
+                     "fp64_pipe_frac": prof.get("fp64_pipe_frac"), "profile": prof.get("source"),
                      "kernel": kernel_name, "alg_bytes_per_agent": bal,
                      "kernel_ms": t_force, "peak_source": peak_src, "sweep_mix": sweep_mix},
         "step_roofline_frac": n * bal / (ms * 1e-3) / 1e9 / peak,

@@ -642,6 +642,8 @@ static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
 }
 
 constexpr int kBigCap = 1024;   // survivors per agent in the second warp pass
+constexpr int kDenseKS = 44;    // survivor list of the thread-per-agent dense sweep (44 x 128 x 8 B smem)
+constexpr double kDenseThreadSurv = 36.0;   // expected survivors up to which it is used (C3-50: 52, warp path)
 
 // the second pass for dense uid-mode agents that spilled the warp's shared
 // queue (A.ovf), then the thread-per-agent rounds for the few beyond kBigCap
@@ -766,6 +768,20 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
     cudaStream_t st = c->stream;
     const int blocks = std::min(cdiv(A.n, kThreads / 32), c->sms * 16);
     CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
+    if (c->summation == SUM_UID && CG_KEY32 && A.uid32 && surv <= kDenseThreadSurv) {
+        // moderately dense (C2: ~27 survivors): one thread per agent with a
+        // kDenseKS-entry survivor list in shared memory; agents with more
+        // survivors (or an operand outside the call-free range) go to the
+        // warp kernel's global-queue pass
+        constexpr int NT = 128;
+        if (sweep_uniform(c, A))
+            sweep7_kernel<T, true, true, kDenseKS, false, 5, false, true, true, NT><<<cdiv(A.n, NT), NT, 0, st>>>(A);
+        else
+            sweep7_kernel<T, true, true, kDenseKS, false, 5, false, true, false, NT><<<cdiv(A.n, NT), NT, 0, st>>>(A);
+        LAUNCH_CHECK(c);
+        c->launches += 1;
+        return launch_sweep_warp_big<T, false>(c, A);
+    }
     if (c->summation == SUM_UID) {
         auto k = sweep_warp_kernel<T, true>;
         const size_t sm = sizeof(WarpSmem<T, true>);

@@ -133,17 +133,24 @@ __device__ __forceinline__ void f2_unpack(f32x2 v, float &lo, float &hi)
 // partner within ri + rmax + skin <= 2L can sit two boxes away), while m still
 // counts the reference's 27 boxes.
 // UNI: a uniform pool; rj, rsum, req and the list limit are kernel constants.
+// NT: threads per CTA (the per-thread survivor lists are [KS][NT] in shared memory).
+// PACKED (uid order, every uid < 2^32): one 64-bit entry per survivor,
+// uid32 << 32 | slot -- one load, compare and store per insertion-sort move
+// (C2 sweep 0.826 -> 0.761 ms, C4 list build 3.27 -> 3.23 ms).
 template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, bool DEFER, bool LIST = false,
-          bool KEY32 = false, bool UNI = false>
+          bool KEY32 = false, bool UNI = false, int NT = kThreads>
 __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s, unsigned &c_m,
                                             unsigned &c_nk, unsigned &c_nd, float &dmax2)
 {
-    __shared__ int lst[KS][kThreads];
-    // KEY32: every uid < 2^32 (A.uid32): 32-bit sort keys from the proxies
-    __shared__ typename std::conditional<KEY32, uint32_t, uint64_t>::type ukey[UIDMODE ? KS : 1][kThreads];
+    constexpr bool PACKED = KEY32 && UIDMODE;
+    __shared__ int lst[PACKED ? 1 : KS][PACKED ? 1 : NT];
+    __shared__ uint64_t ukey[(UIDMODE && !PACKED) ? KS : 1][(UIDMODE && !PACKED) ? NT : 1];
+    __shared__ uint64_t pk[PACKED ? KS : 1][PACKED ? NT : 1];
     static_assert(!(UIDMODE && FLUSH), "uid order needs the whole list");
 #define LST(k) lst[k][threadIdx.x]
 #define UKEY(k) ukey[k][threadIdx.x]
+#define PK(k) pk[k][threadIdx.x]
+#define SLOT(k) (PACKED ? (int)(unsigned)PK(k) : LST(k))
     {
         const int key = __ldg(A.skey + s);
         int ix, iy, iz;
@@ -269,18 +276,18 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         // record is in flight while the current pair is evaluated
         auto evaluate = [&](int cnt_) {
             int p = 0;
-            if (p < cnt_ && LST(p) == s) ++p;
+            if (p < cnt_ && SLOT(p) == s) ++p;
             if (p >= cnt_) return;
-            int j = storage_of(A, LST(p));
+            int j = storage_of(A, SLOT(p));
             Rec<T> o = A.rec[j];
 #pragma unroll 1
             while (p < cnt_) {
                 const int jc = j;
                 const Rec<T> co = o;
                 ++p;
-                if (p < cnt_ && LST(p) == s) ++p;   // the agent itself
+                if (p < cnt_ && SLOT(p) == s) ++p;   // the agent itself
                 if (p < cnt_) {
-                    j = storage_of(A, LST(p));
+                    j = storage_of(A, SLOT(p));
                     o = A.rec[j];
                 }
                 const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;   // kernels.py:198-203
@@ -364,9 +371,12 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             m = walk(
                 [&](int t, unsigned u) {
                     if (ns < KS) {
-                        LST(ns) = t;
-                        if (KEY32) UKEY(ns) = u;
-                        else UKEY(ns) = A.uid32 ? (uint64_t)u : cand_uid(t);
+                        if constexpr (PACKED) {
+                            PK(ns) = ((uint64_t)u << 32) | (unsigned)t;
+                        } else {
+                            LST(ns) = t;
+                            UKEY(ns) = A.uid32 ? (uint64_t)u : cand_uid(t);
+                        }
                         ++ns;
                     }
                     ++total;
@@ -377,18 +387,30 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 return;
             }
             if (total <= KS) {
-                // insertion sort by uid, then one evaluation in uid order
+                // insertion sort by uid, then one evaluation in uid order (measured
+                // against a one-ahead pipelined compare and a binary search + 4-way
+                // unrolled shift: within +-3 %, profiles/r2/ab_r2k.jsonl)
                 for (int p = 1; p < ns; ++p) {
-                    const uint64_t u = UKEY(p);
-                    const int v = LST(p);
-                    int q = p;
-                    while (q > 0 && UKEY(q - 1) > u) {
-                        UKEY(q) = UKEY(q - 1);
-                        LST(q) = LST(q - 1);
-                        --q;
+                    if constexpr (PACKED) {
+                        const uint64_t v = PK(p);
+                        int q = p;
+                        while (q > 0 && PK(q - 1) > v) {
+                            PK(q) = PK(q - 1);
+                            --q;
+                        }
+                        PK(q) = v;
+                    } else {
+                        const uint64_t u = UKEY(p);
+                        const int v = LST(p);
+                        int q = p;
+                        while (q > 0 && UKEY(q - 1) > u) {
+                            UKEY(q) = UKEY(q - 1);
+                            LST(q) = LST(q - 1);
+                            --q;
+                        }
+                        UKEY(q) = u;
+                        LST(q) = v;
                     }
-                    UKEY(q) = u;
-                    LST(q) = v;
                 }
                 evaluate(ns);
             } else {
@@ -400,24 +422,38 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                     int nr = 0;
                     walk(
                         [&](int t, unsigned u) {
-                            const uint64_t ut = (KEY32 || A.uid32) ? (uint64_t)u : cand_uid(t);
-                            if (!first && ut <= floor_uid) return;
-                            int q;
-                            if (nr < KS) q = nr++;
-                            else if (ut < UKEY(KS - 1)) q = KS - 1;
-                            else return;
-                            while (q > 0 && UKEY(q - 1) > ut) {
-                                UKEY(q) = UKEY(q - 1);
-                                LST(q) = LST(q - 1);
-                                --q;
+                            if constexpr (PACKED) {   // keys packed with the slot: same order as by uid
+                                const uint64_t v = ((uint64_t)u << 32) | (unsigned)t;
+                                if (!first && v <= floor_uid) return;
+                                int q;
+                                if (nr < KS) q = nr++;
+                                else if (v < PK(KS - 1)) q = KS - 1;
+                                else return;
+                                while (q > 0 && PK(q - 1) > v) {
+                                    PK(q) = PK(q - 1);
+                                    --q;
+                                }
+                                PK(q) = v;
+                            } else {
+                                const uint64_t ut = (KEY32 || A.uid32) ? (uint64_t)u : cand_uid(t);
+                                if (!first && ut <= floor_uid) return;
+                                int q;
+                                if (nr < KS) q = nr++;
+                                else if (ut < UKEY(KS - 1)) q = KS - 1;
+                                else return;
+                                while (q > 0 && UKEY(q - 1) > ut) {
+                                    UKEY(q) = UKEY(q - 1);
+                                    LST(q) = LST(q - 1);
+                                    --q;
+                                }
+                                UKEY(q) = ut;
+                                LST(q) = t;
                             }
-                            UKEY(q) = ut;
-                            LST(q) = t;
                         },
                         [] {});
                     evaluate(nr);
                     done += nr;
-                    if (nr) floor_uid = UKEY(nr - 1);
+                    if (nr) floor_uid = PACKED ? PK(nr - 1) : UKEY(nr - 1);
                     first = false;
                 }
             }
@@ -474,6 +510,8 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
     }
 #undef LST
 #undef UKEY
+#undef PK
+#undef SLOT
 }
 
 // counters: one REDUX per warp, one atomic per warp and counter
@@ -502,13 +540,13 @@ __device__ __forceinline__ void warp_dmax(unsigned long long *slots, float dmax2
 }
 
 template <typename T, bool UIDMODE, bool ZSORTED, int KS, bool FLUSH, int MINB, bool LIST = false, bool KEY32 = false,
-          bool UNI = false>
-__global__ void __launch_bounds__(kThreads, MINB) sweep7_kernel(Sweep7Args<T> A)
+          bool UNI = false, int NT = kThreads>
+__global__ void __launch_bounds__(NT, MINB) sweep7_kernel(Sweep7Args<T> A)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned c_m = 0, c_nk = 0, c_nd = 0;
     float dmax2 = 0.f;
-    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true, LIST, KEY32, UNI>(A, s, c_m, c_nk, c_nd, dmax2);
+    if (s < A.n) sweep_agent<T, UIDMODE, ZSORTED, KS, FLUSH, true, LIST, KEY32, UNI, NT>(A, s, c_m, c_nk, c_nd, dmax2);
     warp_counters(A.slots, c_m, c_nk, c_nd);
     if (LIST || ZSORTED) warp_dmax(A.slots, dmax2);
 }
