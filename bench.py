@@ -418,7 +418,6 @@ EXTRAS = (   # (key, config, precision, summation, list skin, sort_every, freeze
     ("c4_lists_off", "c4", "fp64", "uid", 0, 1, False),     # the literal "grid rebuild each step"
     ("c2_fp64", "c2", "fp64", "uid", -1, 1, False),
     ("c2_fp32", "c2", "fp32", "uid", -1, 1, False),
-    ("c2_fp64_stencil_sum", "c2", "fp64", "stencil", -1, 1, False),
     ("c3_4_sorted", "c3_4", "fp64", "uid", -1, 1, True),
     ("c3_4_unsorted", "c3_4", "fp64", "uid", -1, 0, True),
     ("c3_27_sorted", "c3_27", "fp64", "uid", -1, 1, True),

@@ -184,7 +184,7 @@ def test_c4_chained_steps_match_oracle(cuda_required, c4):
 
 
 @pytest.mark.parametrize("sort", [True, False], ids=["sorted", "unsorted"])
-@pytest.mark.parametrize("density", [4.0, 100.0])
+@pytest.mark.parametrize("density", [4.0, 27.0, 100.0])
 def test_c3_full_size_matches_oracle(cuda_required, density, sort):
     import oracle
     from paper_2105_00039_b200 import _native as N
