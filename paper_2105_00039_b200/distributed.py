@@ -218,38 +218,46 @@ class SlabRunner:
         self.rec = ctx.record_bytes
         self.sync_counters = sync_counters
         self._pending = []
-        self._epoch = None           # (list epoch, cached receive counts)
+        self._epoch = None           # per list epoch: sizes, counters and the send buffer (fixed within it)
+        self._has_epoch = hasattr(ctx, "slab_list_epoch")
+        self._overlap = hasattr(ctx, "slab_step_interior") and getattr(exchange, "stream", None) is not None
+        self._deferred = not sync_counters and hasattr(ctx, "fetch_stats")
+
+    def _sizes(self, counts, recv_counts):
+        W, R = self.world, self.rec
+        c3, r3 = counts.reshape(W, 3), recv_counts.reshape(W, 3)
+        send_bytes, recv_bytes = c3.sum(1) * R, r3.sum(1) * R
+        return {"recv_counts": recv_counts, "send_bytes": send_bytes, "recv_bytes": recv_bytes,
+                "send": self.ex.buffer(int(send_bytes.sum())), "migrated_in": int(r3[:, 0].sum()),
+                "migrated_out": int(c3[:, 0].sum()), "ghosts": int(r3[:, 1:].sum()),
+                "recv_any": bool(recv_bytes.sum() > 0)}
 
     def step(self, params5, flags=0, interaction_radius=None, box_cap=1 << 24):
-        ctx, ex, r, W, R = self.ctx, self.ex, self.rank, self.world, self.rec
+        ctx, ex, r, W = self.ctx, self.ex, self.rank, self.world
         bb = ex.allreduce_bbox(ctx.local_bbox())
         counts, planes = ctx.slab_plan(bb, W, r, interaction_radius, box_cap)
-        epoch = ctx.slab_list_epoch() if hasattr(ctx, "slab_list_epoch") else -1
+        epoch = ctx.slab_list_epoch() if self._has_epoch else -1
         if epoch >= 0 and self._epoch is not None and self._epoch[0] == epoch:
-            recv_counts = self._epoch[1]                  # refresh sizes are fixed within an epoch
+            z = self._epoch[1]          # refresh sizes (and the send buffer) are fixed within an epoch
         else:
-            recv_counts = ex.alltoall_counts(counts)      # 3 per rank pair
-            self._epoch = (epoch, recv_counts) if epoch >= 0 else None
-        send_bytes = counts.reshape(W, 3).sum(1) * R
-        recv_bytes = recv_counts.reshape(W, 3).sum(1) * R
-        send = ex.buffer(int(send_bytes.sum()))
+            z = self._sizes(counts, ex.alltoall_counts(counts))   # 3 counts per rank pair
+            self._epoch = (epoch, z) if epoch >= 0 else None
+        send = z["send"]
         ctx.slab_pack(ex.ptr(send))
-        if (epoch >= 0 and recv_bytes.sum() > 0 and hasattr(ctx, "slab_step_interior")
-                and getattr(ex, "stream", None) is not None):
+        if epoch >= 0 and z["recv_any"] and self._overlap:
             # list step: the interior agents' sweep runs while the ghost refresh
             # is in flight (side stream); the boundary agents follow the unpack
             after = ex.record_event()
             ctx.slab_step_interior(params5, flags)
-            recv, done = ex.exchange_async(send, send_bytes, recv_bytes, after)
+            recv, done = ex.exchange_async(send, z["send_bytes"], z["recv_bytes"], after)
             ex.wait_event(done)
         else:
-            recv = ex.alltoall_bytes(send, send_bytes, recv_bytes)
-        ctx.slab_unpack(ex.ptr(recv), recv_counts)
-        rc = recv_counts.reshape(W, 3)
+            recv = ex.alltoall_bytes(send, z["send_bytes"], z["recv_bytes"])
+        ctx.slab_unpack(ex.ptr(recv), z["recv_counts"])
         stats = SlabStats(force_evals=0, candidates=0, degenerate_pairs=0, agents=0,
-                          migrated_in=int(rc[:, 0].sum()), migrated_out=int(counts.reshape(W, 3)[:, 0].sum()),
-                          ghosts=int(rc[:, 1:].sum()), planes=(int(planes[0]), int(planes[1])))
-        if not self.sync_counters and hasattr(ctx, "fetch_stats"):
+                          migrated_in=z["migrated_in"], migrated_out=z["migrated_out"], ghosts=z["ghosts"],
+                          planes=(int(planes[0]), int(planes[1])))
+        if self._deferred:
             # enqueue only: the counters are fetched (and all-reduced) in collect()
             self._pending.append((stats, ctx.slab_step(params5, flags, wait=False)))
             return stats
