@@ -59,6 +59,9 @@ extern "C" {
 #define CG_OPT_LIST_SKIN 6      /* neighbour-list reuse on the sparse path: -1 = auto (skin 0.07 x box
                                    length, default), 0 = off, k > 0 = skin of k/1000 length units.
                                    Results are identical with or without it (csrc/list.cuh). */
+#define CG_OPT_INNER_LIST 7     /* second-level list on the sparse path: k = 0 off, k > 0 = a sub-list of the
+                                   partners within r_i + r_j + (k/1000) x skin, rebuilt from the neighbour
+                                   list while the motion allows (default 500) -- identical results */
 
 typedef struct cg_context cg_context;
 
@@ -160,8 +163,10 @@ int cg_unit_vectors(cg_context *ctx, int64_t n, const uint64_t *uid, int64_t ste
 
 /* Neighbour-list reuse counters (CG_OPT_LIST_SKIN): out[0] list builds,
  * out[1] steps served from lists, out[2] lists currently valid, out[3] skin of
- * the last build in 1e-6 length units. */
-int cg_list_stats(cg_context *ctx, int64_t out[5]);
+ * the last build in 1e-6 length units, out[4] slab list steps whose interior
+ * sweep overlapped the ghost refresh, out[5] list steps that swept the
+ * sub-list (CG_OPT_INNER_LIST). */
+int cg_list_stats(cg_context *ctx, int64_t out[6]);
 
 /* ---- radius queries: kernels.grid_neighbor_counts /
  * grid_neighbor_fill (kernels.py:427-520) behind spatial.neighbor_counts /

@@ -22,6 +22,7 @@ CG_ERR_POOL_CAPACITY, CG_ERR_CUDA, CG_ERR_NO_DEVICE, CG_ERR_STATE = 4, 5, 6, 7
 CG_FP64, CG_FP32 = 0, 1
 CG_STEP_SORT, CG_STEP_FREEZE, CG_STEP_RECORD = 1, 2, 4
 CG_OPT_SUMMATION, CG_OPT_SWEEP, CG_OPT_RELAYOUT_EVERY, CG_OPT_PATH, CG_OPT_LIST_SKIN = 1, 3, 4, 5, 6
+CG_OPT_INNER_LIST = 7
 
 # every symbol include/cellgrid_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_last_error",
@@ -279,11 +280,12 @@ class Context:
 
     def list_stats(self):
         """(builds, list steps, valid, skin, slab list steps with the interior
-        sweep overlapping the ghost refresh) of the neighbour-list reuse."""
-        out = np.zeros(5, np.int64)
+        sweep overlapping the ghost refresh, list steps that swept the
+        sub-list) of the neighbour-list reuse."""
+        out = np.zeros(6, np.int64)
         check(load().cg_list_stats(self.h, ptr(out)), self.h)
         return {"builds": int(out[0]), "list_steps": int(out[1]), "valid": bool(out[2]),
-                "skin": out[3] * 1e-6, "overlapped": int(out[4])}
+                "skin": out[3] * 1e-6, "overlapped": int(out[4]), "inner_steps": int(out[5])}
 
     # ---- radius queries (spatial.neighbor_counts / neighbor_csr)
     def neighbor_counts(self, radius):

@@ -146,6 +146,13 @@ struct cg_context {
     // neighbour-list reuse (list.cuh): skin < 0 = auto (0.07 x box length), 0 = off
     double list_skin = -1.0;
     int *nbr = nullptr, *nbr_n = nullptr;
+    // second-level list (list.cuh INNER): partners within r_i + r_j + delta
+    int *inbr = nullptr, *inbr_n = nullptr;
+    double inner_frac = 0.5;      // delta = inner_frac x skin (CG_OPT_INNER_LIST / 1000); 0 = off
+    bool inner_valid = false, inner_written = false;
+    int64_t inner_epoch = -1;     // list_builds when the sub-list was written
+    double inner_D = 0.0, inner_delta = 0.0;
+    int64_t inner_steps = 0;      // list steps that swept the sub-list
     int64_t nbr_cap = 0;
     int nbr_width = 0;            // entries per agent allocated
     int list_width = kListCap;    // entries per agent of the current lists
@@ -238,6 +245,14 @@ static int fail(cg_context *c, int code, const char *fmt, ...)
 
 #define LAUNCH_CHECK(ctx) CUDA_TRY(ctx, cudaGetLastError())
 
+static void free_inner(cg_context *c)
+{
+    if (c->inbr) cudaFree(c->inbr);
+    if (c->inbr_n) cudaFree(c->inbr_n);
+    c->inbr = c->inbr_n = nullptr;
+    c->inner_valid = false;
+}
+
 static void free_agents(cg_context *c)
 {
     Buffers &b = c->b;
@@ -255,6 +270,7 @@ static void free_agents(cg_context *c)
     if (c->nbr) cudaFree(c->nbr);
     if (c->nbr_n) cudaFree(c->nbr_n);
     c->nbr = c->nbr_n = nullptr;
+    free_inner(c);
     c->nbr_cap = 0;
     c->list_valid = false;
     c->last_kind = 0;
@@ -302,6 +318,7 @@ static int grow_agents(cg_context *c, int64_t cap)
     c->cap = 0;
     int *nbr = c->nbr, *nbr_n = c->nbr_n;
     c->nbr = c->nbr_n = nullptr;
+    free_inner(c);
     int rc = alloc_agents(c, cap);
     if (nbr) cudaFree(nbr);
     if (nbr_n) cudaFree(nbr_n);
@@ -929,10 +946,15 @@ static int ensure_lists(cg_context *c, int width)
     if (c->nbr) cudaFree(c->nbr);
     if (c->nbr_n) cudaFree(c->nbr_n);
     c->nbr = c->nbr_n = nullptr;
+    free_inner(c);
     c->nbr_cap = 0;
     c->nbr_width = 0;
     CUDA_TRY(c, cudaMalloc(&c->nbr, sizeof(int) * (size_t)width * (size_t)c->cap));
     CUDA_TRY(c, cudaMalloc(&c->nbr_n, sizeof(int) * (size_t)c->cap));
+    if (width == kListCap) {   // the sub-list: sparse pools only (dense widths would double a large buffer)
+        CUDA_TRY(c, cudaMalloc(&c->inbr, sizeof(int) * (size_t)width * (size_t)c->cap));
+        CUDA_TRY(c, cudaMalloc(&c->inbr_n, sizeof(int) * (size_t)c->cap));
+    }
     c->nbr_cap = c->cap;
     c->nbr_width = width;
     return CG_OK;
@@ -972,11 +994,17 @@ static void list_account(cg_context *c)
             c->list_wait = c->list_backoff;
         }
     }
+    if (c->inner_written) {   // the sub-list reflects the positions before the last step's move
+        c->inner_D = 0.0;
+        c->inner_written = false;
+    }
     if (c->list_valid && c->last_kind != 0 && !c->last_freeze) {
         double M = 0.0;
         for (int q = 0; q < 6; ++q) M = std::max(M, std::fabs(c->bbox_host[q]));
         const double ulp = M * (sizeof(T) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07);
-        c->list_D += std::sqrt(std::max(c->bbox_host[7], 0.0)) * (1.0 + 1e-6) + 2.0 * ulp;
+        const double dD = std::sqrt(std::max(c->bbox_host[7], 0.0)) * (1.0 + 1e-6) + 2.0 * ulp;
+        c->list_D += dD;
+        c->inner_D += dD;
     }
 }
 
@@ -1001,7 +1029,15 @@ static void launch_list_sweep(cg_context *c, ListArgs<T> &A, int n, bool fused, 
 {
     const bool uni = list_uniform<T>(c, A);
     const int nblk = cdiv(n, kListThreads);
-    if (fused) {
+    if (fused && A.inner) {   // also write the sub-list (fused steps only)
+        if (uni) {
+            const T ro = A.u_rsum + A.inner_delta;
+            A.u_inner_bound = ro * ro * (T)1.00000095367431640625;
+            list_sweep_kernel<T, true, true, true><<<nblk, kListThreads, 0, st>>>(A);
+        } else {
+            list_sweep_kernel<T, true, false, true><<<nblk, kListThreads, 0, st>>>(A);
+        }
+    } else if (fused) {
         if (uni) list_sweep_kernel<T, true, true><<<nblk, kListThreads, 0, st>>>(A);
         else list_sweep_kernel<T, true><<<nblk, kListThreads, 0, st>>>(A);
     } else {
@@ -1052,6 +1088,25 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     A.nbr = c->nbr;
     A.nbr_n = c->nbr_n;
     A.nbr_stride = c->nbr_cap;
+    // the sub-list (list.cuh INNER): swept while twice the motion since it was
+    // written stays below its delta; otherwise the whole list is swept and a
+    // new sub-list written
+    const bool inner_on = fused && c->inbr && c->inner_frac > 0.0 && c->list_width == kListCap;
+    const bool use_inner = inner_on && c->inner_valid && c->inner_epoch == c->list_builds &&
+                           2.0 * c->inner_D <= 0.999 * c->inner_delta;
+    if (use_inner) {
+        A.nbr = c->inbr;
+        A.nbr_n = c->inbr_n;
+        c->inner_steps++;
+    } else if (inner_on) {
+        c->inner_delta = c->inner_frac * c->list_skin_used;
+        A.inner = c->inbr;
+        A.inner_n = c->inbr_n;
+        A.inner_delta = (T)c->inner_delta;
+        c->inner_valid = true;
+        c->inner_written = true;
+        c->inner_epoch = c->list_builds;
+    }
     A.disp_x = (T *)c->b.disp[0];
     A.disp_y = (T *)c->b.disp[1];
     A.disp_z = (T *)c->b.disp[2];
@@ -2149,6 +2204,11 @@ int cg_set_option(cg_context *c, int key, int value)
         c->path = value;
         return CG_OK;
     }
+    if (key == CG_OPT_INNER_LIST && value >= 0) {
+        c->inner_frac = value * 1e-3;
+        c->inner_valid = false;
+        return CG_OK;
+    }
     if (key == CG_OPT_LIST_SKIN && value >= -1) {
         c->list_skin = value < 0 ? -1.0 : value * 1e-3;
         c->list_valid = false;
@@ -2753,7 +2813,7 @@ int cg_unit_vectors(cg_context *c, int64_t n, const uint64_t *uid, int64_t step,
     return CG_OK;
 }
 
-int cg_list_stats(cg_context *c, int64_t out[5])
+int cg_list_stats(cg_context *c, int64_t out[6])
 {
     if (!c || !out) return CG_ERR_VALUE;
     out[0] = c->list_builds;
@@ -2761,6 +2821,7 @@ int cg_list_stats(cg_context *c, int64_t out[5])
     out[2] = c->list_valid ? 1 : 0;
     out[3] = (int64_t)llround(c->list_skin_used * 1e6);
     out[4] = c->overlapped_steps;
+    out[5] = c->inner_steps;
     return CG_OK;
 }
 

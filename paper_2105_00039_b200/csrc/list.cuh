@@ -52,6 +52,10 @@ struct ListArgs {
     // the pool dtype with the kernel's expressions -- rsum = ri + ri,
     // req = (ri * ri) / rsum, bound = rsum * rsum * reject_factor
     T u_rsum, u_req, u_bound;
+    // INNER: the sub-list written while sweeping the neighbour list -- every
+    // entry with s2 <= (rsum + inner_delta)^2 (1 + 2^-20), in list order
+    int *inner, *inner_n;
+    T inner_delta, u_inner_bound;   // u_inner_bound: UNI
 };
 
 template <typename T>
@@ -140,7 +144,12 @@ __device__ __forceinline__ float reject_factor<float>() { return 1.00000048f; }
 // UNI: a uniform pool -- rj, rsum, the rejection bound and req are kernel
 // constants (bitwise the values the per-pair expressions give), which frees
 // the registers of the per-partner cache and three FP64 operations per entry.
-template <typename T, bool FUSED = false, bool UNI = false>
+//
+// INNER: also write the sub-list of the entries within rsum + inner_delta (a
+// superset test on s2): the next list steps sweep it instead of the whole
+// list while twice the motion since stays below inner_delta (two-level
+// Verlet list: fewer loop iterations per warp, same pairs, same order).
+template <typename T, bool FUSED = false, bool UNI = false, bool INNER = false>
 __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(ListArgs<T> A)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -203,9 +212,11 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
         int jnn = cnt > 1 ? __ldg(L + A.nbr_stride) : 0;
         Rec<T> o;
         if (cnt > 0) o = A.rec[jn];
+        int ni = 0;   // INNER: entries written
 #pragma unroll 1
         for (int p = 0; p < cnt; ++p) {
             const Rec<T> co = o;
+            const int jc = jn;
             jn = jnn;
             if (p + 1 < cnt) o = A.rec[jn];
             if (p + 2 < cnt) jnn = __ldg(L + (p + 2) * A.nbr_stride);
@@ -213,6 +224,13 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
             const T rj = UNI ? zero : co.d * half;
             const T s2 = dx * dx + dy * dy + dz * dz;
             const T rsum = UNI ? A.u_rsum : ri + rj;
+            if (INNER) {
+                const T ro = rsum + A.inner_delta;
+                if (!(s2 > (UNI ? A.u_inner_bound : ro * ro * T(1.00000095367431640625)))) {
+                    A.inner[(long long)ni * A.nbr_stride + a] = jc;
+                    ++ni;
+                }
+            }
             if (s2 > (UNI ? A.u_bound : rsum * rsum * kfac)) continue;
             const T dist = tsqrt_nocall(s2, ok);
             const T delta = rsum - dist;
@@ -230,6 +248,13 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
             fy = fy + sc * dy;
             fz = fz + sc * dz;
             if (!ok) break;   // (measured: without the break ptxas allocates worse, 1.25 vs 1.16 ms)
+        }
+        if (INNER) {
+            if (!ok) {   // the loop stopped early: the rest of the list goes to the sub-list unfiltered
+                for (int p = 0; p < cnt; ++p) A.inner[(long long)p * A.nbr_stride + a] = __ldg(L + p * A.nbr_stride);
+                ni = cnt;
+            }
+            A.inner_n[a] = ni;
         }
         if (!ok) {
             const AgentSum<T> S = list_agent_slow<T>(A.rec, A.uid, L, A.nbr_stride, cnt, a, A.p.kappa, A.p.gamma,

@@ -24,6 +24,8 @@ makers = {"c1": lambda: workloads.c1(pm), "c2": lambda: workloads.c2(pm), "c4": 
 pool = makers.get(base, lambda: workloads.c3(float(base[3:]), pm))()
 ctx = _native.Context(0, pool.dtype)
 ctx.set_option(_native.CG_OPT_LIST_SKIN, int(os.environ.get("SKIN", "-1")))
+if os.environ.get("INNER"):
+    ctx.set_option(_native.CG_OPT_INNER_LIST, int(os.environ["INNER"]))
 ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
 flags = _native.CG_STEP_SORT | (_native.CG_STEP_FREEZE if os.environ.get("FREEZE") else 0)
 kinds, tot, force, evals = [], [], [], []
@@ -45,4 +47,5 @@ out["evals_last"] = evals[-1]
 out["evals_hash"] = int(np.sum(np.array(evals, dtype=np.int64) * np.arange(1, steps + 1)))
 got = ctx.download()
 out["pos_hash"] = float(np.sum(got["px"] * 1.0 + got["py"] * 2.0 + got["pz"] * 3.0))
+out["list_stats"] = ctx.list_stats()
 print(json.dumps(out), flush=True)
