@@ -41,6 +41,9 @@
 #ifndef CG_LIST_BUILD_MINB
 #define CG_LIST_BUILD_MINB 4   // the same sweep building neighbour lists
 #endif
+#ifndef CG_LIST_BUILD_KS
+#define CG_LIST_BUILD_KS 16    // survivors per agent held by the (uniform, 32-bit key) list build
+#endif
 #ifndef CG_SPARSE_MINB
 #define CG_SPARSE_MINB 4   // resident 256-thread CTAs per SM for the sparse sweep (measured)
 #endif
@@ -143,12 +146,12 @@ struct cg_context {
     bool last_record = false;
     bool last_dense = false;
     bool grid_current = false;    // the grid indexes the stored positions (cg_build_grid)
-    // neighbour-list reuse (list.cuh): skin < 0 = auto (0.07 x box length), 0 = off
+    // neighbour-list reuse (list.cuh): skin < 0 = auto (auto_skin), 0 = off
     double list_skin = -1.0;
     int *nbr = nullptr, *nbr_n = nullptr;
     // second-level list (list.cuh INNER): partners within r_i + r_j + delta
     int *inbr = nullptr, *inbr_n = nullptr;
-    double inner_frac = 0.5;      // delta = inner_frac x skin (CG_OPT_INNER_LIST / 1000); 0 = off
+    double inner_frac = 0.29;     // delta = inner_frac x skin (CG_OPT_INNER_LIST / 1000); 0 = off
     bool inner_valid = false, inner_written = false;
     int64_t inner_epoch = -1;     // list_builds when the sub-list was written
     double inner_D = 0.0, inner_delta = 0.0;
@@ -207,6 +210,7 @@ struct cg_context {
         bool split_ok = false;
         int b_lo = 0, b_hi = 0;
         bool interior_done = false;
+        bool use_inner = false, write_inner = false;   // this list step's sub-list choice (both parts)
         double x_lo_abs = 0, x_hi_abs = 0;   // the owned slab's x range at the rebuild
         int64_t ref_counts[kHist] = {};      // refresh records per (destination, kind)
         int64_t ref_total = 0;
@@ -532,6 +536,19 @@ static int materialize_presentation(cg_context *c, cudaStream_t st = nullptr)
     return CG_OK;
 }
 
+// Automatic skin: sparse pools (48-wide lists) 0.12 L -- builds every ~19
+// C4 steps, the two-level list keeps the swept lists short; dense pools
+// 0.07 L (their list width grows with (d + skin)^3).  Measured at C4 over 60
+// steps (profiles/r2/ab_r2m..r.jsonl): skin 0.7 / 1.2 / 1.3 / 1.5 with the
+// sub-list at r_i + r_j + 0.35 -> 1.300 / 1.213 / 1.231 / 1.309 ms per step;
+// beyond 1.3 the build's survivors overflow its 16-entry lists.
+static double auto_skin(const cg_context *c, const Geometry &g)
+{
+    const double surv = 4.19 * (double)c->n / (double)g.nb;
+    const bool dense = c->path == 2 || (c->path == 0 && surv > 10.0);
+    return (dense ? 0.07 : 0.12) * g.L;
+}
+
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
 // idx (or, when relayout, the records in slot order in the alternate buffers).
 static int ensure_big(cg_context *c);
@@ -626,7 +643,7 @@ static int build_grid_geo(cg_context *c, const Geometry &g, bool relayout, bool 
     if (step_path && dense && (rc = ensure_big(c))) return rc;   // the warp sweep's second-pass queues
     if (step_path && dense && c->list_skin != 0.0 && c->sweep_impl == 1 && c->n > 1) {
         // the lists a later build will need, allocated now (outside the build step)
-        const int w = list_width_for(c, g, c->list_skin < 0 ? 0.07 * g.L : c->list_skin);
+        const int w = list_width_for(c, g, c->list_skin < 0 ? auto_skin(c, g) : c->list_skin);
         if (w > 0 && (rc = ensure_lists(c, w))) return rc;
     }
     if (relayout) {
@@ -736,9 +753,9 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         if (!c->last_dense) {
             const int g1 = cdiv(A.n, kThreads), g2 = std::min(cdiv(A.n, kThreads), c->sms * 2);
             if (CG_KEY32 && A.uid32 && sweep_uniform(c, A)) {
-                sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true, true, true>
+                sweep7_kernel<T, true, false, CG_LIST_BUILD_KS, false, CG_LIST_BUILD_MINB, true, true, true>
                     <<<g1, kThreads, 0, st>>>(A);
-                sweep7_overflow<T, true, false, 16, true, true><<<g2, kThreads, 0, st>>>(A);
+                sweep7_overflow<T, true, false, CG_LIST_BUILD_KS, true, true><<<g2, kThreads, 0, st>>>(A);
             } else if (CG_KEY32 && A.uid32) {
                 sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true, true><<<g1, kThreads, 0, st>>>(A);
                 sweep7_overflow<T, true, false, 16, true, true><<<g2, kThreads, 0, st>>>(A);
@@ -1279,7 +1296,7 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
         bool build = lists_on && c->list_wait == 0;
         if (c->list_wait > 0) c->list_wait--;
         if (build) {
-            c->list_skin_used = c->list_skin < 0 ? 0.07 * g.L : c->list_skin;
+            c->list_skin_used = c->list_skin < 0 ? auto_skin(c, g) : c->list_skin;
             build = c->list_skin_used > 0 && c->list_skin_used <= g.L;
             c->list_width = build ? list_width_for(c, g, c->list_skin_used) : 0;
             build = build && c->list_width > 0;
@@ -1792,6 +1809,28 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
     A.nbr = c->nbr;
     A.nbr_n = c->nbr_n;
     A.nbr_stride = c->nbr_cap;
+    // the sub-list (list.cuh INNER), chosen once per step for both parts
+    if (part == 1 || !S.interior_done) {
+        const bool inner_on = fused && c->inbr && c->inner_frac > 0.0 && c->list_width == kListCap;
+        S.use_inner = inner_on && c->inner_valid && c->inner_epoch == c->list_builds &&
+                      2.0 * c->inner_D <= 0.999 * c->inner_delta;
+        S.write_inner = inner_on && !S.use_inner;
+        if (S.use_inner) c->inner_steps++;
+        if (S.write_inner) {
+            c->inner_delta = c->inner_frac * c->list_skin_used;
+            c->inner_valid = true;
+            c->inner_written = true;
+            c->inner_epoch = c->list_builds;
+        }
+    }
+    if (S.use_inner) {
+        A.nbr = c->inbr;
+        A.nbr_n = c->inbr_n;
+    } else if (S.write_inner) {
+        A.inner = c->inbr;
+        A.inner_n = c->inbr_n;
+        A.inner_delta = (T)c->inner_delta;
+    }
     A.disp_x = (T *)c->b.disp[0] - rot;
     A.disp_y = (T *)c->b.disp[1] - rot;
     A.disp_z = (T *)c->b.disp[2] - rot;
@@ -1911,7 +1950,7 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
             if (build) {
                 if ((rc = ensure_lists(c, kListCap))) return rc;
                 c->list_width = kListCap;
-                c->list_skin_used = c->list_skin < 0 ? 0.07 * S.g.L : c->list_skin;
+                c->list_skin_used = c->list_skin < 0 ? 0.12 * S.g.L : c->list_skin;   // slab lists are 48 wide
                 build = c->list_skin_used > 0 && c->list_skin_used <= S.g.L;
             }
             if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
