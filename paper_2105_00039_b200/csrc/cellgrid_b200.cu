@@ -968,7 +968,7 @@ static int ensure_lists(cg_context *c, int width)
     c->nbr_width = 0;
     CUDA_TRY(c, cudaMalloc(&c->nbr, sizeof(int) * (size_t)width * (size_t)c->cap));
     CUDA_TRY(c, cudaMalloc(&c->nbr_n, sizeof(int) * (size_t)c->cap));
-    if (width == kListCap) {   // the sub-list: sparse pools only (dense widths would double a large buffer)
+    if (2.0 * (double)width * (double)c->cap * 4.0 <= 16e9) {   // the sub-list, same width (within the 16 GB list budget)
         CUDA_TRY(c, cudaMalloc(&c->inbr, sizeof(int) * (size_t)width * (size_t)c->cap));
         CUDA_TRY(c, cudaMalloc(&c->inbr_n, sizeof(int) * (size_t)c->cap));
     }
@@ -1108,7 +1108,7 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     // the sub-list (list.cuh INNER): swept while twice the motion since it was
     // written stays below its delta; otherwise the whole list is swept and a
     // new sub-list written
-    const bool inner_on = fused && c->inbr && c->inner_frac > 0.0 && c->list_width == kListCap;
+    const bool inner_on = fused && c->inbr && c->inner_frac > 0.0;
     const bool use_inner = inner_on && c->inner_valid && c->inner_epoch == c->list_builds &&
                            2.0 * c->inner_D <= 0.999 * c->inner_delta;
     if (use_inner) {
@@ -1811,7 +1811,7 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
     A.nbr_stride = c->nbr_cap;
     // the sub-list (list.cuh INNER), chosen once per step for both parts
     if (part == 1 || !S.interior_done) {
-        const bool inner_on = fused && c->inbr && c->inner_frac > 0.0 && c->list_width == kListCap;
+        const bool inner_on = fused && c->inbr && c->inner_frac > 0.0;
         S.use_inner = inner_on && c->inner_valid && c->inner_epoch == c->list_builds &&
                       2.0 * c->inner_D <= 0.999 * c->inner_delta;
         S.write_inner = inner_on && !S.use_inner;
