@@ -676,7 +676,16 @@ static int launch_sweep7_k(cg_context *c, const Sweep7Args<T> &A)
 }
 
 constexpr int kBigCap = 1024;   // survivors per agent in the second warp pass
-constexpr int kDenseKS = 44;    // survivor list of the thread-per-agent dense sweep (44 x 128 x 8 B smem)
+// dense thread sweep: survivors per agent in shared memory and 128-thread CTAs
+// per SM (36 x 128 x 8 B = 36 KB: 6 CTAs; measured C2 sweep 44/5: 0.828 ms,
+// 36/6: 0.776 ms, 32/7: 1.073 ms -- too many agents overflow to the warp pass)
+#ifndef CG_DENSE_KS
+#define CG_DENSE_KS 36
+#endif
+#ifndef CG_DENSE_MINB
+#define CG_DENSE_MINB 6
+#endif
+constexpr int kDenseKS = CG_DENSE_KS;    // survivor list of the thread-per-agent dense sweep
 constexpr double kDenseThreadSurv = 36.0;   // expected survivors up to which it is used (C3-50: 52, warp path)
 
 // the second pass for dense uid-mode agents that spilled the warp's shared
@@ -811,9 +820,9 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         // stencil-order warp sweep (C2 0.76 vs 1.29 ms)
         constexpr int NT = 128;
         if (sweep_uniform(c, A))
-            sweep7_kernel<T, true, true, kDenseKS, false, 5, false, true, true, NT><<<cdiv(A.n, NT), NT, 0, st>>>(A);
+            sweep7_kernel<T, true, true, kDenseKS, false, CG_DENSE_MINB, false, true, true, NT><<<cdiv(A.n, NT), NT, 0, st>>>(A);
         else
-            sweep7_kernel<T, true, true, kDenseKS, false, 5, false, true, false, NT><<<cdiv(A.n, NT), NT, 0, st>>>(A);
+            sweep7_kernel<T, true, true, kDenseKS, false, CG_DENSE_MINB, false, true, false, NT><<<cdiv(A.n, NT), NT, 0, st>>>(A);
         LAUNCH_CHECK(c);
         c->launches += 1;
         return launch_sweep_warp_big<T, false>(c, A);
