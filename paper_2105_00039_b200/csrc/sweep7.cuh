@@ -366,10 +366,12 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
             }
         } else {
             auto cand_uid = [&](int t) -> uint64_t { return A.uid[storage_of(A, t)]; };
-            // first walk: keep the first KS survivors, count all of them
+            // first walk: keep the first KS survivors, count all of them (the
+            // agent itself is not one: nothing to sort or skip later)
             int ns = 0, total = 0;
             m = walk(
                 [&](int t, unsigned u) {
+                    if (t == s) return;
                     if (ns < KS) {
                         if constexpr (PACKED) {
                             PK(ns) = ((uint64_t)u << 32) | (unsigned)t;
@@ -422,6 +424,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                     int nr = 0;
                     walk(
                         [&](int t, unsigned u) {
+                            if (t == s) return;
                             if constexpr (PACKED) {   // keys packed with the slot: same order as by uid
                                 const uint64_t v = ((uint64_t)u << 32) | (unsigned)t;
                                 if (!first && v <= floor_uid) return;
