@@ -1055,6 +1055,11 @@ static void launch_list_sweep(cg_context *c, ListArgs<T> &A, int n, bool fused, 
 {
     const bool uni = list_uniform<T>(c, A);
     const int nblk = cdiv(n, kListThreads);
+    if (fused) {   // agents off the call-free range are deferred to list_slow_kernel
+        A.ovf = c->b.ovf;
+        A.ovf_count = c->ovf_count;
+        cudaMemsetAsync(c->ovf_count, 0, sizeof(unsigned), st);
+    }
     if (fused && A.inner) {   // also write the sub-list (fused steps only)
         if (uni) {
             const T ro = A.u_rsum + A.inner_delta;
@@ -1069,6 +1074,10 @@ static void launch_list_sweep(cg_context *c, ListArgs<T> &A, int n, bool fused, 
     } else {
         if (uni) list_sweep_kernel<T, false, true><<<nblk, kListThreads, 0, st>>>(A);
         else list_sweep_kernel<T><<<nblk, kListThreads, 0, st>>>(A);
+    }
+    if (fused) {
+        list_slow_kernel<T><<<c->sms, kThreads, 0, st>>>(A);
+        c->launches += 1;
     }
 }
 

@@ -56,6 +56,10 @@ struct ListArgs {
     // entry with s2 <= (rsum + inner_delta)^2 (1 + 2^-20), in list order
     int *inner, *inner_n;
     T inner_delta, u_inner_bound;   // u_inner_bound: UNI
+    // FUSED: agents whose operands leave the call-free range (or coincident
+    // centres) are deferred here and finished by list_slow_kernel
+    int *ovf;
+    unsigned *ovf_count;
 };
 
 template <typename T>
@@ -130,6 +134,50 @@ template <>
 __device__ __forceinline__ double reject_factor<double>() { return 1.0000000000009095; }
 template <>
 __device__ __forceinline__ float reject_factor<float>() { return 1.00000048f; }
+
+// _write_displacement (kernels.py:266-277) and apply (engine.py:325-327) of
+// one agent, the next step's bbox shell and the largest displacement.
+// NOCALL: the norm and the cap division call-free (common.cuh); false = an
+// operand left their range, nothing written (the agent is deferred).
+template <typename T, bool NOCALL>
+__device__ __forceinline__ bool list_finish(const ListArgs<T> &A, int a, T xi, T yi, T zi, T di, T fx, T fy, T fz,
+                                            float &dmax2)
+{
+    const T zero = A.p.zero;
+    bool ok = true;
+    const T n2 = fx * fx + fy * fy + fz * fz;
+    const T norm = NOCALL ? (n2 == zero ? zero : tsqrt_nocall(n2, ok)) : tsqrt<T>(n2);
+    T ddx = zero, ddy = zero, ddz = zero;
+    if (!(norm <= A.p.adh_scale * A.adh[a])) {
+        T sc = A.p.timestep;
+        if (norm * sc > A.p.max_disp) sc = NOCALL ? tdiv_nocall(A.p.max_disp, norm, ok) : A.p.max_disp / norm;
+        ddx = fx * sc;
+        ddy = fy * sc;
+        ddz = fz * sc;
+    }
+    if (NOCALL && !ok) return false;
+    A.disp_x[a] = ddx;
+    A.disp_y[a] = ddy;
+    A.disp_z[a] = ddz;
+    dmax2 = fmaxf(dmax2, (float)((double)ddx * ddx + (double)ddy * ddy + (double)ddz * ddz));
+    if (A.new_rec) {
+        const T nxp = xi + ddx, nyp = yi + ddy, nzp = zi + ddz;
+        Rec<T> nr;
+        nr.x = nxp;
+        nr.y = nyp;
+        nr.z = nzp;
+        nr.d = di;
+        A.new_rec[a] = nr;
+        const double p3[3] = {(double)nxp, (double)nyp, (double)nzp};
+        unsigned long long *slot = A.slots + (blockIdx.x % kSlots) * kSlotWords;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (p3[q] <= A.shell_lo[q]) atomicMin(slot + q, enc_ordered(p3[q]));
+            if (p3[q] >= A.shell_hi[q]) atomicMax(slot + 3 + q, enc_ordered(p3[q]));
+        }
+    }
+    return true;
+}
 
 // FUSED: the step's box counting is done here (box id of the current
 // position, one atomic per run of equal keys in the warp) instead of in a
@@ -256,54 +304,59 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
             }
             A.inner_n[a] = ni;
         }
-        if (!ok) {
-            const AgentSum<T> S = list_agent_slow<T>(A.rec, A.uid, L, A.nbr_stride, cnt, a, A.p.kappa, A.p.gamma,
-                                                     zero);
-            fx = S.fx;
-            fy = S.fy;
-            fz = S.fz;
-            nk = S.nk;
-            nd = S.nd;
-        }
-        // _write_displacement, kernels.py:266-277
-        const T norm = tsqrt<T>(fx * fx + fy * fy + fz * fz);
-        T ddx = zero, ddy = zero, ddz = zero;
-        if (!(norm <= A.p.adh_scale * A.adh[a])) {
-            T sc = A.p.timestep;
-            if (norm * sc > A.p.max_disp) sc = A.p.max_disp / norm;
-            ddx = fx * sc;
-            ddy = fy * sc;
-            ddz = fz * sc;
-        }
-        A.disp_x[a] = ddx;
-        A.disp_y[a] = ddy;
-        A.disp_z[a] = ddz;
-        dmax2 = (float)((double)ddx * ddx + (double)ddy * ddy + (double)ddz * ddz);
-        if (A.new_rec) {
-            const T nxp = xi + ddx, nyp = yi + ddy, nzp = zi + ddz;
-            Rec<T> nr;
-            nr.x = nxp;
-            nr.y = nyp;
-            nr.z = nzp;
-            nr.d = me.d;
-            A.new_rec[a] = nr;
-            const double p3[3] = {(double)nxp, (double)nyp, (double)nzp};
-            unsigned long long *slot = A.slots + (blockIdx.x % kSlots) * kSlotWords;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                if (p3[q] <= A.shell_lo[q]) atomicMin(slot + q, enc_ordered(p3[q]));
-                if (p3[q] >= A.shell_hi[q]) atomicMax(slot + 3 + q, enc_ordered(p3[q]));
+        bool done = true;
+        // fp64 FUSED: no call in the pair loop or the finish -- an agent off the
+        // fast range is finished by list_slow_kernel (spills 32 -> 8 bytes, list
+        // step 1.035 -> 1.010 ms at C4); fp32 keeps the inline slow path (its
+        // fused kernel measured 0.947 -> 1.083 ms with the deferral)
+        constexpr bool DEFER_SLOW = FUSED && sizeof(T) == 8;
+        if (DEFER_SLOW) {
+            done = ok && list_finish<T, true>(A, a, xi, yi, zi, me.d, fx, fy, fz, dmax2);
+            if (!done) A.ovf[atomicAdd(A.ovf_count, 1u)] = a;
+        } else {
+            if (!ok) {
+                const AgentSum<T> S = list_agent_slow<T>(A.rec, A.uid, L, A.nbr_stride, cnt, a, A.p.kappa,
+                                                         A.p.gamma, zero);
+                fx = S.fx;
+                fy = S.fy;
+                fz = S.fz;
+                nk = S.nk;
+                nd = S.nd;
+            }
+            list_finish<T, false>(A, a, xi, yi, zi, me.d, fx, fy, fz, dmax2);
+            if (!FUSED && A.rec_m) {
+                A.rec_m[a] = m;
+                A.rec_nk[a] = nk;
             }
         }
-        if (!FUSED && A.rec_m) {
-            A.rec_m[a] = m;
-            A.rec_nk[a] = nk;
-        }
+        if (!done) nk = nd = 0;   // counted by list_slow_kernel
         c_m = FUSED ? 0u : (unsigned)m;
         c_nk = (unsigned)nk;
         c_nd = (unsigned)nd;
     }
     warp_counters(A.slots, c_m, c_nk, c_nd);
+    warp_dmax(A.slots, dmax2);
+}
+
+// The agents a FUSED list sweep deferred (A.ovf): the whole pair sum with the
+// library's sqrt and division and the coincident-centre branch, then the
+// same finish -- rare (extreme operands, coincident centres), grid-stride.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) list_slow_kernel(ListArgs<T> A)
+{
+    unsigned c_nk = 0, c_nd = 0;
+    float dmax2 = 0.f;
+    const unsigned cnt_ovf = *A.ovf_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt_ovf; k += gridDim.x * blockDim.x) {
+        const int a = A.ovf[k];
+        const Rec<T> me = A.rec[a];
+        const AgentSum<T> S = list_agent_slow<T>(A.rec, A.uid, A.nbr + a, A.nbr_stride, A.nbr_n[a], a, A.p.kappa,
+                                                 A.p.gamma, A.p.zero);
+        list_finish<T, false>(A, a, me.x, me.y, me.z, me.d, S.fx, S.fy, S.fz, dmax2);
+        c_nk += (unsigned)S.nk;
+        c_nd += (unsigned)S.nd;
+    }
+    warp_counters(A.slots, 0u, c_nk, c_nd);
     warp_dmax(A.slots, dmax2);
 }
 

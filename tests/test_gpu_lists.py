@@ -330,3 +330,25 @@ def test_very_dense_pools_match_oracle(cuda_required, n, density, skin):
     if skin:
         assert kinds[:3] == [0, 1, 2], kinds
     ctx.close()
+
+
+@pytest.mark.parametrize("fp32", [False, True], ids=["fp64", "fp32"])
+def test_coincident_centres_on_list_steps(cuda_required, fp32):
+    """Frozen pool with 200 exactly coincident pairs: every list step meets
+    dist == 0, which leaves the call-free arithmetic (fp64: the agent is
+    deferred to list_slow_kernel; fp32: the inline slow path) -- counters,
+    degenerate pairs and every column equal the list-free run."""
+    from paper_2105_00039_b200.pool import AgentPool, PrecisionMode
+    from paper_2105_00039_b200.workloads import jittered_lattice_positions
+    pos = jittered_lattice_positions(20, 8.0, 1.0, 4)
+    pool = AgentPool.from_arrays(np.vstack([pos, pos[::40]]), 10.0, 0.4,
+                                 PrecisionMode.FP32 if fp32 else PrecisionMode.FP64)
+    frozen = tuple(range(8))
+    got, st = _run(pool, -1, 8, 0, freeze_at=frozen, record=False)
+    ref, _ = _run(pool, 0, 8, 0, freeze_at=frozen, record=False)
+    assert st["list_steps"] > 0, st
+    assert got[-1][0][2] > 0   # degenerate pairs on the list steps
+    for k, (a, b) in enumerate(zip(got, ref)):
+        assert a[0] == b[0], k
+        for col in a[1]:
+            assert np.array_equal(a[1][col], b[1][col]), (k, col)
