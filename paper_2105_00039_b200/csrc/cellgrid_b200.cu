@@ -35,9 +35,6 @@
 
 #include "../../include/cellgrid_b200.h"
 
-#ifndef CG_KEY32
-#define CG_KEY32 1   // sparse sweeps: 32-bit uid sort keys when every uid < 2^32 (0: 64-bit)
-#endif
 #ifndef CG_LIST_BUILD_MINB
 #define CG_LIST_BUILD_MINB 4   // the same sweep building neighbour lists
 #endif
@@ -761,11 +758,11 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
         if (!c->last_dense) {
             const int g1 = cdiv(A.n, kThreads), g2 = std::min(cdiv(A.n, kThreads), c->sms * 2);
-            if (CG_KEY32 && A.uid32 && sweep_uniform(c, A)) {
+            if (A.uid32 && sweep_uniform(c, A)) {
                 sweep7_kernel<T, true, false, CG_LIST_BUILD_KS, false, CG_LIST_BUILD_MINB, true, true, true>
                     <<<g1, kThreads, 0, st>>>(A);
                 sweep7_overflow<T, true, false, CG_LIST_BUILD_KS, true, true><<<g2, kThreads, 0, st>>>(A);
-            } else if (CG_KEY32 && A.uid32) {
+            } else if (A.uid32) {
                 sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true, true><<<g1, kThreads, 0, st>>>(A);
                 sweep7_overflow<T, true, false, 16, true, true><<<g2, kThreads, 0, st>>>(A);
             } else {
@@ -795,9 +792,9 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
         // sparse: survivors summed in uid order (deterministic and bit-identical to
         // the reference whatever the slot order in a box); agents with more than
         // 16 survivors go to the overflow kernel
-        if (CG_KEY32 && A.uid32 && sweep_uniform(c, A))
+        if (A.uid32 && sweep_uniform(c, A))
             return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB, true, true>(c, A);
-        if (CG_KEY32 && A.uid32) return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB, true>(c, A);
+        if (A.uid32) return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB, true>(c, A);
         return launch_sweep7_k<T, true, false, 16, false, CG_SPARSE_MINB>(c, A);
     }
     // moderately dense (<= 20 expected survivors): one thread per agent
@@ -811,7 +808,7 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
     cudaStream_t st = c->stream;
     const int blocks = std::min(cdiv(A.n, kThreads / 32), c->sms * 16);
     CUDA_TRY(c, cudaMemsetAsync(A.ovf_count, 0, sizeof(unsigned), st));
-    if (CG_KEY32 && A.uid32 && surv <= kDenseThreadSurv) {
+    if (A.uid32 && surv <= kDenseThreadSurv) {
         // moderately dense (C2: ~27 survivors): one thread per agent with a
         // kDenseKS-entry survivor list in shared memory; agents with more
         // survivors (or an operand outside the call-free range) go to the

@@ -31,9 +31,6 @@ namespace cg {
 #ifndef CG_WARP_MINB
 #define CG_WARP_MINB 4       // stencil-mode blocks per SM (uid mode: 3, shared-memory bound)
 #endif
-#ifndef CG_WARP_REG_SORT
-#define CG_WARP_REG_SORT 1   // 0: every uid sort in shared memory (A/B switch)
-#endif
 constexpr int kWarpQ = 256;   // survivors queued per warp before a flush (stencil mode)
 
 template <typename T, bool UIDMODE>
@@ -334,8 +331,7 @@ __global__ void __launch_bounds__(kThreads, UIDMODE ? 3 : CG_WARP_MINB) sweep_wa
             // registers up to 256 survivors, else in shared memory
             uint64_t *U = BIG ? A.big_u + (size_t)gw * A.big_cap : S.u[wid];
             const bool packed = A.uid32;
-            if (!CG_WARP_REG_SORT) {
-            } else if (packed && qn <= 64) {
+            if (packed && qn <= 64) {
                 sort_queue_packed<2>(Q, qn, lane, A.prox.p);
                 np2 = 0;
             } else if (packed && qn <= 128) {
