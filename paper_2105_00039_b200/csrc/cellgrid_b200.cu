@@ -1034,7 +1034,8 @@ static void list_account(cg_context *c)
 // Uniform pool: the list sweep's pair constants (list.cuh UNI), in the pool
 // dtype with the kernel's expression order (host: -ffp-contract=off, SSE).
 // fp64 only (C4 list sweep 1.159 -> 1.040 ms, C3-27 0.465 -> 0.403 ms; the
-// fp32 kernel measured 0.921 -> 0.940 ms, profiles/r2/ab_r2g.jsonl).
+// fp32 kernel measured 0.921 -> 0.940 ms, profiles/r2/ab_r2g.jsonl, and again
+// 0.870 -> 0.892 ms after the early loads, ab_r2aa.jsonl).
 template <typename T>
 static bool list_uniform(const cg_context *c, ListArgs<T> &A)
 {
