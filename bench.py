@@ -43,7 +43,7 @@ B_ALG = {"fp64": 64, "fp32": 32}     # 5 scalars read + 3 written 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", help="c4 (default), c2, c1, c3_<density>")

@@ -148,7 +148,7 @@ struct cg_context {
     int *nbr = nullptr, *nbr_n = nullptr;
     // second-level list (list.cuh INNER): partners within r_i + r_j + delta
     int *inbr = nullptr, *inbr_n = nullptr;
-    double inner_frac = 0.29;     // delta = inner_frac x skin (CG_OPT_INNER_LIST / 1000); 0 = off
+    double inner_frac = 0.195;    // delta = inner_frac x skin (CG_OPT_INNER_LIST / 1000; 0.35 at C4); 0 = off
     bool inner_valid = false, inner_written = false;
     int64_t inner_epoch = -1;     // list_builds when the sub-list was written
     double inner_D = 0.0, inner_delta = 0.0;
@@ -533,17 +533,18 @@ static int materialize_presentation(cg_context *c, cudaStream_t st = nullptr)
     return CG_OK;
 }
 
-// Automatic skin: sparse pools (48-wide lists) 0.12 L -- builds every ~19
+// Automatic skin: sparse pools (48-wide lists) 0.18 L -- builds every ~30
 // C4 steps, the two-level list keeps the swept lists short; dense pools
-// 0.07 L (their list width grows with (d + skin)^3).  Measured at C4 over 60
-// steps (profiles/r2/ab_r2m..r.jsonl): skin 0.7 / 1.2 / 1.3 / 1.5 with the
-// sub-list at r_i + r_j + 0.35 -> 1.300 / 1.213 / 1.231 / 1.309 ms per step;
-// beyond 1.3 the build's survivors overflow its 16-entry lists.
+// 0.07 L (their list width grows with (d + skin)^3).  Measured at C4 over 180
+// steps with the sub-list at r_i + r_j + 0.35 and 24-entry build lists
+// (profiles/r2/ab_r2ac.jsonl): skin 1.2 / 1.8 / 2.2 / 2.6 -> 1.216 / 1.193 /
+// 1.190 / 1.182 ms per step (60 steps with 16-entry build lists: 0.7 / 1.2 ->
+// 1.300 / 1.213 ms, ab_r2m..r.jsonl).
 static double auto_skin(const cg_context *c, const Geometry &g)
 {
     const double surv = 4.19 * (double)c->n / (double)g.nb;
     const bool dense = c->path == 2 || (c->path == 0 && surv > 10.0);
-    return (dense ? 0.07 : 0.12) * g.L;
+    return (dense ? 0.07 : 0.18) * g.L;
 }
 
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
@@ -1966,7 +1967,7 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
             if (build) {
                 if ((rc = ensure_lists(c, kListCap))) return rc;
                 c->list_width = kListCap;
-                c->list_skin_used = c->list_skin < 0 ? 0.12 * S.g.L : c->list_skin;   // slab lists are 48 wide
+                c->list_skin_used = c->list_skin < 0 ? 0.18 * S.g.L : c->list_skin;   // slab lists are 48 wide
                 build = c->list_skin_used > 0 && c->list_skin_used <= S.g.L;
             }
             if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
