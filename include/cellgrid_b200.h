@@ -61,7 +61,7 @@ extern "C" {
                                    Results are identical with or without it (csrc/list.cuh). */
 #define CG_OPT_INNER_LIST 7     /* second-level list on the sparse path: k = 0 off, k > 0 = a sub-list of the
                                    partners within r_i + r_j + (k/1000) x skin, rebuilt from the neighbour
-                                   list while the motion allows (default 195) -- identical results */
+                                   list while the motion allows (default 250) -- identical results */
 
 typedef struct cg_context cg_context;
 

@@ -148,7 +148,7 @@ struct cg_context {
     int *nbr = nullptr, *nbr_n = nullptr;
     // second-level list (list.cuh INNER): partners within r_i + r_j + delta
     int *inbr = nullptr, *inbr_n = nullptr;
-    double inner_frac = 0.195;    // delta = inner_frac x skin (CG_OPT_INNER_LIST / 1000; 0.35 at C4); 0 = off
+    double inner_frac = 0.25;     // delta = inner_frac x skin (CG_OPT_INNER_LIST / 1000; 0.45 at C4); 0 = off
     bool inner_valid = false, inner_written = false;
     int64_t inner_epoch = -1;     // list_builds when the sub-list was written
     double inner_D = 0.0, inner_delta = 0.0;
