@@ -8,7 +8,9 @@ size-independent properties:
   order, positions and displacements after steps 1, 5 and 10; step 0
   reproduces the reference's own counters recorded in SURVEY.md 8d
   (109,695,208 evaluations, 890,262,272 candidates, 207^3 boxes);
-* C3 (2M, density 4 and 100, frozen as in benchmark B), with and without the
+* C4 fp32: 5 chained steps (grid sweep, list build, whole-list and sub-list
+  sweeps) equal the oracle's fp32 step;
+* C3 (2M, density 4, 27 and 100, frozen as in benchmark B), with and without the
   Z-order sort, 2 steps: counters, storage order, displacements;
 * C2 (1M random, fp64 and fp32), 3 chained steps: the reference's step-0
   counters and the oracle's pool after every step;
@@ -181,6 +183,29 @@ def test_c4_chained_steps_match_oracle(cuda_required, c4):
     finally:
         ctx.close()
     assert kinds[:3] == [0, 1, 2] and kinds.count(2) >= 5, kinds
+
+
+def test_c4_fp32_chained_steps_match_oracle(cuda_required, c4f):
+    """The fp32 variant at full size: a grid sweep, a list build and list steps
+    (sub-list written, then swept) equal the oracle's fp32 step bit for bit."""
+    import oracle
+    from paper_2105_00039_b200 import _native as N
+    from paper_2105_00039_b200.mechanics import ForceParams
+    ref = c4f.copy()
+    ctx = _bench_ctx(c4f)
+    kinds = []
+    try:
+        for k in range(5):
+            st = ctx.step(PARAMS5, None, 1 << 24, N.CG_STEP_SORT)
+            kinds.append(int(st.sweep_kind))
+            r = oracle.step(ref, ForceParams(), sort=True, threads=ORACLE_THREADS)
+            assert (st.force_evals, st.candidates, st.degenerate_pairs) == (
+                r.force_evals, r.candidates, r.degenerate_pairs), k
+            if k in (1, 4):
+                _same_pool(ctx.download(), ref, ("c4f", k))
+    finally:
+        ctx.close()
+    assert kinds == [0, 1, 2, 2, 2], kinds
 
 
 @pytest.mark.parametrize("sort", [True, False], ids=["sorted", "unsorted"])
