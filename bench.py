@@ -277,10 +277,10 @@ def run_reference(args, rank, world):
         return
     pool, desc = make_pool(args.config, args.precision, side=args.side)
     n = pool.count
-    # bounded sample: the full workload while K+W full steps fit in ~3 min, else fewer steps
+    # bounded sample: the full workload for as many of the K steps as fit in ~1 min of CPU time
     t_one, th = cpu_port_run(pool, args.precision, 1, args.sort_every, args.freeze)
     k_total = args.steps + args.warmup
-    k_run = max(1, min(args.steps, int(180.0 / max(t_one, 1e-3)) - 1))
+    k_run = max(1, min(args.steps, int(60.0 / max(t_one, 1e-3)) - 1))
     t_med, th = cpu_port_run(pool, args.precision, k_run, args.sort_every, args.freeze)
     v = n / t_med
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
