@@ -56,12 +56,15 @@ extern "C" {
 #define CG_OPT_RELAYOUT_EVERY 4 /* move the records into slot order on every k-th sort step (k >= 1, default 1) */
 #define CG_OPT_PATH 5           /* 0 = auto (by agents per box), 1 = sparse (uid-sorted survivor lists),
                                    2 = dense (boxes ordered by (z, uid), CG_OPT_SUMMATION applies) */
-#define CG_OPT_LIST_SKIN 6      /* neighbour-list reuse: -1 = auto (skin 0.18 x box length on sparse pools,
+#define CG_OPT_LIST_SKIN 6      /* neighbour-list reuse: -1 = auto (skin 0.26 x box length on sparse pools,
                                    0.07 on dense ones; default), 0 = off, k > 0 = skin of k/1000 length units.
                                    Results are identical with or without it (csrc/list.cuh). */
 #define CG_OPT_INNER_LIST 7     /* second-level list on the sparse path: k = 0 off, k > 0 = a sub-list of the
                                    partners within r_i + r_j + (k/1000) x skin, rebuilt from the neighbour
-                                   list while the motion allows (default 250) -- identical results */
+                                   list while the motion allows (default 173) -- identical results */
+#define CG_OPT_MID_LIST 8       /* optional middle level: k > 0 = a sub-list within r_i + r_j + (k/1000) x skin
+                                   written from the neighbour list, from which the short sub-list is refreshed
+                                   (default 385; 0 = off) -- identical results */
 
 typedef struct cg_context cg_context;
 

@@ -22,7 +22,7 @@ CG_ERR_POOL_CAPACITY, CG_ERR_CUDA, CG_ERR_NO_DEVICE, CG_ERR_STATE = 4, 5, 6, 7
 CG_FP64, CG_FP32 = 0, 1
 CG_STEP_SORT, CG_STEP_FREEZE, CG_STEP_RECORD = 1, 2, 4
 CG_OPT_SUMMATION, CG_OPT_SWEEP, CG_OPT_RELAYOUT_EVERY, CG_OPT_PATH, CG_OPT_LIST_SKIN = 1, 3, 4, 5, 6
-CG_OPT_INNER_LIST = 7
+CG_OPT_INNER_LIST, CG_OPT_MID_LIST = 7, 8
 
 # every symbol include/cellgrid_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = ("cg_abi_version", "cg_device_count", "cg_create", "cg_destroy", "cg_last_error",

@@ -146,13 +146,19 @@ struct cg_context {
     // neighbour-list reuse (list.cuh): skin < 0 = auto (auto_skin), 0 = off
     double list_skin = -1.0;
     int *nbr = nullptr, *nbr_n = nullptr;
-    // second-level list (list.cuh INNER): partners within r_i + r_j + delta
-    int *inbr = nullptr, *inbr_n = nullptr;
-    double inner_frac = 0.25;     // delta = inner_frac x skin (CG_OPT_INNER_LIST / 1000; 0.45 at C4); 0 = off
-    bool inner_valid = false, inner_written = false;
-    int64_t inner_epoch = -1;     // list_builds when the sub-list was written
-    double inner_D = 0.0, inner_delta = 0.0;
-    int64_t inner_steps = 0;      // list steps that swept the sub-list
+    // sub-lists (list.cuh INNER): level k in {1, 2} holds the partners within
+    // r_i + r_j + delta_k, written by a sweep of a longer list (its parent:
+    // level 0 = the neighbour list, or level 1) and swept while twice the
+    // motion since it was written stays below delta_k and its parent is still
+    // valid.  Level 2 is the short list most steps sweep (CG_OPT_INNER_LIST),
+    // level 1 an optional middle list (CG_OPT_MID_LIST) that refreshes it.
+    int *lvl_nbr[3] = {nullptr, nullptr, nullptr}, *lvl_n[3] = {nullptr, nullptr, nullptr};
+    double lvl_frac[3] = {1.0, 0.385, 0.173};   // delta_k = frac_k x skin (C4: 1.0 and 0.45 at skin 2.6)
+    bool lvl_valid[3] = {}, lvl_written[3] = {};
+    int64_t lvl_epoch[3] = {-1, -1, -1};     // list_builds when written
+    double lvl_D[3] = {}, lvl_delta[3] = {};
+    int lvl_parent[3] = {};
+    int64_t inner_steps = 0;      // list steps that swept a sub-list
     int64_t nbr_cap = 0;
     int nbr_width = 0;            // entries per agent allocated
     int list_width = kListCap;    // entries per agent of the current lists
@@ -207,7 +213,7 @@ struct cg_context {
         bool split_ok = false;
         int b_lo = 0, b_hi = 0;
         bool interior_done = false;
-        bool use_inner = false, write_inner = false;   // this list step's sub-list choice (both parts)
+        int read_lvl = 0, write_lvl = -1;   // this list step's sub-list choice (both parts)
         double x_lo_abs = 0, x_hi_abs = 0;   // the owned slab's x range at the rebuild
         int64_t ref_counts[kHist] = {};      // refresh records per (destination, kind)
         int64_t ref_total = 0;
@@ -248,10 +254,12 @@ static int fail(cg_context *c, int code, const char *fmt, ...)
 
 static void free_inner(cg_context *c)
 {
-    if (c->inbr) cudaFree(c->inbr);
-    if (c->inbr_n) cudaFree(c->inbr_n);
-    c->inbr = c->inbr_n = nullptr;
-    c->inner_valid = false;
+    for (int k = 1; k < 3; ++k) {
+        if (c->lvl_nbr[k]) cudaFree(c->lvl_nbr[k]);
+        if (c->lvl_n[k]) cudaFree(c->lvl_n[k]);
+        c->lvl_nbr[k] = c->lvl_n[k] = nullptr;
+        c->lvl_valid[k] = false;
+    }
 }
 
 static void free_agents(cg_context *c)
@@ -533,18 +541,17 @@ static int materialize_presentation(cg_context *c, cudaStream_t st = nullptr)
     return CG_OK;
 }
 
-// Automatic skin: sparse pools (48-wide lists) 0.18 L -- builds every ~30
-// C4 steps, the two-level list keeps the swept lists short; dense pools
-// 0.07 L (their list width grows with (d + skin)^3).  Measured at C4 over 180
-// steps with the sub-list at r_i + r_j + 0.35 and 24-entry build lists
-// (profiles/r2/ab_r2ac.jsonl): skin 1.2 / 1.8 / 2.2 / 2.6 -> 1.216 / 1.193 /
-// 1.190 / 1.182 ms per step (60 steps with 16-entry build lists: 0.7 / 1.2 ->
-// 1.300 / 1.213 ms, ab_r2m..r.jsonl).
+// Automatic skin: sparse pools (48-wide lists) 0.26 L -- builds every ~45
+// C4 steps, the middle and short sub-lists keep the swept lists short; dense
+// pools 0.07 L (their list width grows with (d + skin)^3).  Measured at C4
+// over 180 steps (profiles/r2/ab_r2ac.jsonl, ab_r2aj.jsonl): two levels at
+// skin 1.2 / 1.8 / 2.6 -> 1.216 / 1.188 / 1.179 ms per step; three levels at
+// 2.6 (middle 1.0, short 0.45) -> 1.165 ms.
 static double auto_skin(const cg_context *c, const Geometry &g)
 {
     const double surv = 4.19 * (double)c->n / (double)g.nb;
     const bool dense = c->path == 2 || (c->path == 0 && surv > 10.0);
-    return (dense ? 0.07 : 0.18) * g.L;
+    return (dense ? 0.07 : 0.26) * g.L;
 }
 
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
@@ -975,9 +982,14 @@ static int ensure_lists(cg_context *c, int width)
     c->nbr_width = 0;
     CUDA_TRY(c, cudaMalloc(&c->nbr, sizeof(int) * (size_t)width * (size_t)c->cap));
     CUDA_TRY(c, cudaMalloc(&c->nbr_n, sizeof(int) * (size_t)c->cap));
-    if (2.0 * (double)width * (double)c->cap * 4.0 <= 16e9) {   // the sub-list, same width (within the 16 GB list budget)
-        CUDA_TRY(c, cudaMalloc(&c->inbr, sizeof(int) * (size_t)width * (size_t)c->cap));
-        CUDA_TRY(c, cudaMalloc(&c->inbr_n, sizeof(int) * (size_t)c->cap));
+    // the sub-lists, same width, within the 16 GB list budget (the middle level
+    // only when enabled)
+    double used = (double)width * (double)c->cap * 4.0;
+    for (int k = 2; k >= 1; --k) {
+        if (c->lvl_frac[k] <= 0.0 || used + (double)width * (double)c->cap * 4.0 > 16e9) continue;
+        CUDA_TRY(c, cudaMalloc(&c->lvl_nbr[k], sizeof(int) * (size_t)width * (size_t)c->cap));
+        CUDA_TRY(c, cudaMalloc(&c->lvl_n[k], sizeof(int) * (size_t)c->cap));
+        used += (double)width * (double)c->cap * 4.0;
     }
     c->nbr_cap = c->cap;
     c->nbr_width = width;
@@ -1018,17 +1030,67 @@ static void list_account(cg_context *c)
             c->list_wait = c->list_backoff;
         }
     }
-    if (c->inner_written) {   // the sub-list reflects the positions before the last step's move
-        c->inner_D = 0.0;
-        c->inner_written = false;
-    }
+    for (int k = 1; k < 3; ++k)
+        if (c->lvl_written[k]) {   // a sub-list reflects the positions before the last step's move
+            c->lvl_D[k] = 0.0;
+            c->lvl_written[k] = false;
+        }
     if (c->list_valid && c->last_kind != 0 && !c->last_freeze) {
         double M = 0.0;
         for (int q = 0; q < 6; ++q) M = std::max(M, std::fabs(c->bbox_host[q]));
         const double ulp = M * (sizeof(T) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07);
         const double dD = std::sqrt(std::max(c->bbox_host[7], 0.0)) * (1.0 + 1e-6) + 2.0 * ulp;
         c->list_D += dD;
-        c->inner_D += dD;
+        c->lvl_D[1] += dD;
+        c->lvl_D[2] += dD;
+    }
+}
+
+// Which list a fused list step sweeps and which sub-list it writes (list.cuh
+// INNER): the shortest valid level -- level 2 if it and its parent chain are
+// valid, else level 1, else the neighbour list -- and the next enabled level
+// below the one swept.  A sub-list written from level r holds every partner of
+// r within r_i + r_j + delta; a pair missing from it was either outside delta
+// at the write (safe while 2 D < delta) or missing from r (safe while r is).
+static void choose_levels(cg_context *c, bool fused, int &read, int &write)
+{
+    read = 0;
+    write = -1;
+    if (!fused) return;
+    auto usable = [&](int k) {
+        return c->lvl_nbr[k] && c->lvl_frac[k] > 0.0 && c->lvl_valid[k] && c->lvl_epoch[k] == c->list_builds &&
+               2.0 * c->lvl_D[k] <= 0.999 * c->lvl_delta[k];
+    };
+    const bool ok1 = usable(1);
+    const bool ok2 = usable(2) && (c->lvl_parent[2] == 0 || ok1);
+    read = ok2 ? 2 : ok1 ? 1 : 0;
+    for (int k = read + 1; k <= 2; ++k)
+        if (c->lvl_nbr[k] && c->lvl_frac[k] > 0.0) {
+            write = k;
+            break;
+        }
+    if (read > 0) c->inner_steps++;
+    if (write > 0) {
+        c->lvl_delta[write] = c->lvl_frac[write] * c->list_skin_used;
+        c->lvl_valid[write] = true;
+        c->lvl_written[write] = true;
+        c->lvl_epoch[write] = c->list_builds;
+        c->lvl_parent[write] = read;
+        if (write == 1) c->lvl_valid[2] = c->lvl_valid[2] && c->lvl_parent[2] == 0;   // its children go with it
+    }
+}
+
+template <typename T>
+static void apply_levels(const cg_context *c, ListArgs<T> &A, int read, int write)
+{
+    if (read > 0) {
+        A.nbr = c->lvl_nbr[read];
+        A.nbr_n = c->lvl_n[read];
+    }
+    if (write > 0) {
+        A.inner = c->lvl_nbr[write];
+        A.inner_n = c->lvl_n[write];
+        A.inner_delta = (T)c->lvl_delta[write];
     }
 }
 
@@ -1122,24 +1184,11 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     A.nbr = c->nbr;
     A.nbr_n = c->nbr_n;
     A.nbr_stride = c->nbr_cap;
-    // the sub-list (list.cuh INNER): swept while twice the motion since it was
-    // written stays below its delta; otherwise the whole list is swept and a
-    // new sub-list written
-    const bool inner_on = fused && c->inbr && c->inner_frac > 0.0;
-    const bool use_inner = inner_on && c->inner_valid && c->inner_epoch == c->list_builds &&
-                           2.0 * c->inner_D <= 0.999 * c->inner_delta;
-    if (use_inner) {
-        A.nbr = c->inbr;
-        A.nbr_n = c->inbr_n;
-        c->inner_steps++;
-    } else if (inner_on) {
-        c->inner_delta = c->inner_frac * c->list_skin_used;
-        A.inner = c->inbr;
-        A.inner_n = c->inbr_n;
-        A.inner_delta = (T)c->inner_delta;
-        c->inner_valid = true;
-        c->inner_written = true;
-        c->inner_epoch = c->list_builds;
+    // the shortest valid sub-list is swept, the next one written (choose_levels)
+    {
+        int rd, wr;
+        choose_levels(c, fused, rd, wr);
+        apply_levels<T>(c, A, rd, wr);
     }
     A.disp_x = (T *)c->b.disp[0];
     A.disp_y = (T *)c->b.disp[1];
@@ -1826,28 +1875,9 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
     A.nbr = c->nbr;
     A.nbr_n = c->nbr_n;
     A.nbr_stride = c->nbr_cap;
-    // the sub-list (list.cuh INNER), chosen once per step for both parts
-    if (part == 1 || !S.interior_done) {
-        const bool inner_on = fused && c->inbr && c->inner_frac > 0.0;
-        S.use_inner = inner_on && c->inner_valid && c->inner_epoch == c->list_builds &&
-                      2.0 * c->inner_D <= 0.999 * c->inner_delta;
-        S.write_inner = inner_on && !S.use_inner;
-        if (S.use_inner) c->inner_steps++;
-        if (S.write_inner) {
-            c->inner_delta = c->inner_frac * c->list_skin_used;
-            c->inner_valid = true;
-            c->inner_written = true;
-            c->inner_epoch = c->list_builds;
-        }
-    }
-    if (S.use_inner) {
-        A.nbr = c->inbr;
-        A.nbr_n = c->inbr_n;
-    } else if (S.write_inner) {
-        A.inner = c->inbr;
-        A.inner_n = c->inbr_n;
-        A.inner_delta = (T)c->inner_delta;
-    }
+    // the sub-lists (choose_levels), chosen once per step for both parts
+    if (part == 1 || !S.interior_done) choose_levels(c, fused, S.read_lvl, S.write_lvl);
+    apply_levels<T>(c, A, S.read_lvl, S.write_lvl);
     A.disp_x = (T *)c->b.disp[0] - rot;
     A.disp_y = (T *)c->b.disp[1] - rot;
     A.disp_z = (T *)c->b.disp[2] - rot;
@@ -1967,7 +1997,7 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
             if (build) {
                 if ((rc = ensure_lists(c, kListCap))) return rc;
                 c->list_width = kListCap;
-                c->list_skin_used = c->list_skin < 0 ? 0.18 * S.g.L : c->list_skin;   // slab lists are 48 wide
+                c->list_skin_used = c->list_skin < 0 ? 0.26 * S.g.L : c->list_skin;   // slab lists are 48 wide
                 build = c->list_skin_used > 0 && c->list_skin_used <= S.g.L;
             }
             if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
@@ -2260,9 +2290,18 @@ int cg_set_option(cg_context *c, int key, int value)
         c->path = value;
         return CG_OK;
     }
+    if (key == CG_OPT_MID_LIST && value >= 0) {
+        c->lvl_frac[1] = value * 1e-3;
+        c->lvl_valid[1] = c->lvl_valid[2] = false;
+        c->list_valid = false;
+        c->nbr_width = 0;   // the list buffers are reallocated (with or without this level) at the next build
+        return CG_OK;
+    }
     if (key == CG_OPT_INNER_LIST && value >= 0) {
-        c->inner_frac = value * 1e-3;
-        c->inner_valid = false;
+        c->lvl_frac[2] = value * 1e-3;
+        c->lvl_valid[2] = false;
+        c->list_valid = false;
+        c->nbr_width = 0;   // the list buffers are reallocated at the next build
         return CG_OK;
     }
     if (key == CG_OPT_LIST_SKIN && value >= -1) {

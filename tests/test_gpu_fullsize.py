@@ -127,7 +127,7 @@ def test_c4_long_run_lists_change_nothing(cuda_required, c4, c4f, prec):
             runs.append((counters, ctx.download(), ctx.list_stats()))
         finally:
             ctx.close()
-    assert runs[0][2]["builds"] >= 10 and runs[0][2]["list_steps"] >= 200, runs[0][2]
+    assert runs[0][2]["builds"] >= 5 and runs[0][2]["list_steps"] >= 200, runs[0][2]
     assert runs[0][0] == runs[1][0]
     for col in runs[0][1]:
         assert np.array_equal(runs[0][1][col], runs[1][1][col]), col

@@ -159,8 +159,8 @@ def test_step_download_equals_step_then_download(cuda_required, name, pool, sort
 
 def test_lists_long_run_matches_oracle(cuda_required):
     """60 chained uid-order steps of a 32,768-agent jittered lattice (several
-    list epochs and rebuilds): lists on (with and without the sub-list of
-    CG_OPT_INNER_LIST), lists off and the C oracle agree bit for bit at the end
+    list epochs and rebuilds): lists on (three levels, two levels, the
+    neighbour list alone), lists off and the C oracle agree bit for bit at the end
     (positions, displacements, storage order)."""
     from paper_2105_00039_b200 import _native as N
     from paper_2105_00039_b200.mechanics import ForceParams
@@ -170,12 +170,15 @@ def test_lists_long_run_matches_oracle(cuda_required):
     params = ForceParams(timestep=0.02)
     p5 = np.array([params.kappa, params.gamma, params.timestep, params.max_displacement, params.adherence_scale])
     outs = []
-    for skin, inner in ((-1, None), (-1, 0), (0, None)):
+    # defaults (three levels), the short sub-list only, no sub-lists, no lists
+    for skin, inner, mid in ((-1, None, None), (-1, None, 0), (-1, 0, 0), (0, None, None)):
         ctx = N.Context(0, pool.dtype)
         ctx.set_option(N.CG_OPT_SUMMATION, 0)
         ctx.set_option(N.CG_OPT_LIST_SKIN, skin)
         if inner is not None:
             ctx.set_option(N.CG_OPT_INNER_LIST, inner)
+        if mid is not None:
+            ctx.set_option(N.CG_OPT_MID_LIST, mid)
         ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
         sts = [ctx.step(p5, None, 1 << 24, N.CG_STEP_SORT) for _ in range(60)]
         evals = [(s.force_evals, s.candidates, s.degenerate_pairs, s.grid_occupied_boxes, s.grid_max_occupancy)
@@ -183,14 +186,15 @@ def test_lists_long_run_matches_oracle(cuda_required):
         outs.append((evals, ctx.download(), ctx.list_stats()))
         ctx.close()
     assert outs[0][2]["builds"] >= 3 and outs[0][2]["list_steps"] >= 30, outs[0][2]
-    assert outs[0][2]["inner_steps"] > 0 and outs[1][2]["inner_steps"] == 0, (outs[0][2], outs[1][2])
+    assert outs[0][2]["inner_steps"] > 0 and outs[1][2]["inner_steps"] > 0 and outs[2][2]["inner_steps"] == 0, \
+        [o[2] for o in outs]
     ref = pool.copy()
     ref_evals = []
     for _ in range(60):
         r = oracle.step(ref, params, sort=True, threads=8)
         ref_evals.append((r.force_evals, r.candidates, r.degenerate_pairs, int(np.count_nonzero(r.box_count)),
                           int(r.box_count.max())))
-    assert outs[0][0] == outs[1][0] == outs[2][0] == ref_evals
+    assert outs[0][0] == outs[1][0] == outs[2][0] == outs[3][0] == ref_evals
     for _, cols, _ in outs:
         assert np.array_equal(cols["uid"], ref.uid)
         for a, b in (("px", "position_x"), ("py", "position_y"), ("pz", "position_z"), ("dx", "displacement_x")):

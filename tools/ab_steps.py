@@ -26,6 +26,8 @@ ctx = _native.Context(0, pool.dtype)
 ctx.set_option(_native.CG_OPT_LIST_SKIN, int(os.environ.get("SKIN", "-1")))
 if os.environ.get("INNER"):
     ctx.set_option(_native.CG_OPT_INNER_LIST, int(os.environ["INNER"]))
+if os.environ.get("MID"):
+    ctx.set_option(_native.CG_OPT_MID_LIST, int(os.environ["MID"]))
 ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
 flags = _native.CG_STEP_SORT | (_native.CG_STEP_FREEZE if os.environ.get("FREEZE") else 0)
 kinds, tot, force, evals = [], [], [], []
