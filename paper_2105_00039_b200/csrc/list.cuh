@@ -299,7 +299,12 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
                 }
             }
             if (s2 > (UNI ? A.u_bound : rsum * rsum * kfac)) continue;
+#if CG_SEEDED_DIV
+            T rs;
+            const T dist = tsqrt_nocall_r(s2, ok, rs);
+#else
             const T dist = tsqrt_nocall(s2, ok);
+#endif
             const T delta = rsum - dist;
             if (!(delta > zero)) continue;
             ++nk;
@@ -310,7 +315,11 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
                 last_req = tdiv_nocall(ri * rj, rsum, ok);
             }
             const T mag = A.p.kappa * delta - A.p.gamma * tsqrt_nocall(last_req * delta, ok);
+#if CG_SEEDED_DIV
+            const T sc = tdiv_seeded(mag, dist, rs, ok);   // dist == 0 (coincident centres): not ok
+#else
             const T sc = tdiv_nocall(mag, dist, ok);   // dist == 0 (coincident centres): not ok
+#endif
             fx = fx + sc * dx;
             fy = fy + sc * dy;
             fz = fz + sc * dz;

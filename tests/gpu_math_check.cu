@@ -2,7 +2,9 @@
 // against the library's IEEE __dsqrt_rn / __ddiv_rn, over random operands
 // spread across the whole exponent range and over the ranges the pair loops
 // see.  Built and run by tests/test_gpu_numerics.py; prints
-// "<checked_sqrt> <fast_sqrt> <bad_sqrt> <checked_div> <fast_div> <bad_div>".
+// "<checked_sqrt> <fast_sqrt> <bad_sqrt> <checked_div> <fast_div> <bad_div>
+//  <checked_seeded> <fast_seeded> <bad_seeded>" -- the last three: a / b for
+// b = sqrt_nocall_r(x) divided with its own rsqrt estimate (div_seeded).
 #include <cstdio>
 #include <cstdint>
 
@@ -35,7 +37,7 @@ __device__ double operand(uint64_t k, int s)
 
 __global__ void check(uint64_t n, unsigned long long *cnt)
 {
-    unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
         const double x = operand(k, 0);
         bool ok = true;
@@ -55,14 +57,28 @@ __global__ void check(uint64_t n, unsigned long long *cnt)
             const double ref = __ddiv_rn(a, b);
             if (__double_as_longlong(q) != __double_as_longlong(ref)) c[5]++;
         }
+        // the pair loops: b = fl(sqrt(s2)), a the force magnitude; x spread
+        // over the whole range and over 2^-40 .. 2^40
+        const double x2 = fabs(operand(k, 3));
+        ok = true;
+        double rs;
+        const double b2 = cg::sqrt_nocall_r(x2, ok, rs);
+        const double a2 = operand(k, 4);
+        const double q2 = cg::div_seeded(a2, b2, rs, ok);
+        c[6]++;
+        if (ok) {
+            c[7]++;
+            const double ref = __ddiv_rn(a2, __dsqrt_rn(x2));
+            if (__double_as_longlong(q2) != __double_as_longlong(ref)) c[8]++;
+        }
     }
-    for (int i = 0; i < 6; ++i) atomicAdd(cnt + i, c[i]);
+    for (int i = 0; i < 9; ++i) atomicAdd(cnt + i, c[i]);
 }
 
 int main(int argc, char **argv)
 {
     const unsigned long long n = argc > 1 ? strtoull(argv[1], nullptr, 10) : (1ull << 30);
-    unsigned long long *d, h[6];
+    unsigned long long *d, h[9];
     cudaMalloc(&d, sizeof h);
     cudaMemset(d, 0, sizeof h);
     check<<<148 * 16, 256>>>(n, d);
@@ -71,6 +87,6 @@ int main(int argc, char **argv)
         printf("cuda error %s\n", cudaGetErrorString(e));
         return 1;
     }
-    printf("%llu %llu %llu %llu %llu %llu\n", h[0], h[1], h[2], h[3], h[4], h[5]);
+    printf("%llu %llu %llu %llu %llu %llu %llu %llu %llu\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8]);
     return 0;
 }
