@@ -2,8 +2,10 @@
 bytes read + written per launch (the bench line's roofline.traffic) and the
 FP64 pipe's busy fraction (roofline.fp64_pipe_frac).
 
-usage: python tools/kernel_metrics.py <config_precision> <kernel name>=<report.ncu-rep> ...
+usage: python tools/kernel_metrics.py <config_precision> <kernel name>=<report.ncu-rep>[@<template>] ...
 e.g.   python tools/kernel_metrics.py c4_fp64 list_sweep_kernel=gpurun_out/prof_list.ncu-rep
+A report holding several launches: @<substring of the kernel name> picks the
+first launch whose name contains it (e.g. "@<double, 1, 1, 0>").
 Entries of other configs / kernels already in the file are kept.
 """
 import csv
@@ -16,10 +18,12 @@ import sys
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "kernel_metrics.json")
 
 
-def metrics(rep):
+def metrics(rep, pick=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    head, units, vals = rows[0], rows[1], rows[2]
+    head, units = rows[0], rows[1]
+    col = head.index("Kernel Name")
+    vals = next(r for r in rows[2:] if pick is None or pick in r[col])
     d = dict(zip(head, vals))
     u = dict(zip(head, units))
 
@@ -43,7 +47,8 @@ def main():
         data = {}
     for arg in sys.argv[2:]:
         name, rep = arg.split("=", 1)
-        m = metrics(rep)
+        rep, _, pick = rep.partition("@")
+        m = metrics(rep, pick or None)
         m["source"] = "ncu --set full --clock-control none, one launch: %s" % os.path.basename(rep)
         data.setdefault(cfg, {})[name] = m
     json.dump(data, open(OUT, "w"), indent=1)
