@@ -78,10 +78,67 @@ class Gpu:
             raise ValueError("relayout_every must be >= 1")
 
 
+@dataclass(frozen=True)
+class Serial:
+    """Reference engine.py:57-59.  The reference states that Serial,
+    AgentParallel and VoxelTiled produce bit-identical pools (engine.py:5);
+    here every one of them is executed by the B200 path in uid summation,
+    which is bit-identical to them (tests/test_gpu_parity.py), so a reference
+    configuration runs unchanged.  The label stays the reference's."""
+
+
+@dataclass(frozen=True)
+class AgentParallel:
+    """Reference engine.py:62-70 (same validation); executed on the B200 (see Serial)."""
+
+    thread_count: int
+
+    def __post_init__(self):
+        if self.thread_count < 1:
+            raise ValueError("thread_count must be >= 1")
+
+
+@dataclass(frozen=True)
+class VoxelTiled:
+    """Reference engine.py:73-87 (same validation); executed on the B200 (see
+    Serial).  The B200 path stages no fixed-capacity tile, so an explicit
+    ``tile_stencil_capacity`` -- whose overflow the reference reports as
+    TileCapacityError -- is not supported and is rejected when the
+    configuration is built."""
+
+    thread_count: int
+    tile_stencil_capacity: Optional[int] = None
+
+    def __post_init__(self):
+        if self.thread_count < 1:
+            raise ValueError("thread_count must be >= 1")
+        if self.tile_stencil_capacity is not None and self.tile_stencil_capacity < 1:
+            raise ValueError("tile_stencil_capacity must be >= 1")
+
+
 def strategy_label(strategy):
+    """Reference engine.py:90-97, plus ``gpu(<device>)`` for Gpu."""
     if isinstance(strategy, Gpu):
         return "gpu(%d)" % strategy.device
+    if isinstance(strategy, Serial):
+        return "serial"
+    if isinstance(strategy, AgentParallel):
+        return "parallel(%d)" % strategy.thread_count
+    if isinstance(strategy, VoxelTiled):
+        return "voxel(%d)" % strategy.thread_count
     raise TypeError("unknown strategy %r" % (strategy,))
+
+
+def as_gpu(strategy):
+    """The Gpu strategy that executes ``strategy``: a reference CPU strategy
+    maps to device 0 in uid summation (bit-identical to it)."""
+    if isinstance(strategy, Gpu):
+        return strategy
+    if isinstance(strategy, VoxelTiled) and strategy.tile_stencil_capacity is not None:
+        raise NotImplementedError("VoxelTiled with an explicit tile_stencil_capacity: the B200 path stages no "
+                                  "fixed-capacity tile; use tile_stencil_capacity=None or Gpu()")
+    strategy_label(strategy)
+    return Gpu(device=0, summation="uid")
 
 
 @dataclass(frozen=True)
@@ -116,7 +173,7 @@ class SimulationConfig:
             raise ValueError("steps must be >= 0")
         if self.morton_sort_every < 0:
             raise ValueError("morton_sort_every must be >= 0 (0 = never)")
-        strategy_label(self.strategy)
+        as_gpu(self.strategy)
 
 
 @dataclass
@@ -181,6 +238,7 @@ _contexts = {}
 
 
 def _context(strategy, dtype):
+    strategy = as_gpu(strategy)
     key = (strategy.device, np.dtype(dtype).str, strategy.summation, strategy.relayout_every)
     ctx = _contexts.get(key)
     if ctx is None:

@@ -146,6 +146,26 @@ def test_public_step_and_run_match_golden(cuda_required):
     assert np.array_equal(pool2.uid, g["s4_out_uid"])
 
 
+@pytest.mark.parametrize("which", ["serial", "parallel", "voxel"])
+def test_reference_strategies_run_on_the_device(cuda_required, which):
+    """A reference configuration with a CPU strategy (Serial / AgentParallel /
+    VoxelTiled, which the reference guarantees bit-identical, engine.py:5)
+    runs unchanged on the B200 path and reproduces the reference's pool."""
+    import paper_2105_00039_b200 as P
+    strat = {"serial": P.Serial(), "parallel": P.AgentParallel(8), "voxel": P.VoxelTiled(8)}[which]
+    g = load_golden("multistep_f64")
+    cfg = P.SimulationConfig(force_params=params_from_golden(g), strategy=strat,
+                             morton_sort_every=int(g["sort_every"]), steps=int(g["steps"]))
+    pool = pool_from_golden(g)
+    rep = P.run(pool, cfg)
+    assert rep.final_state_hash == str(g["state_hash"])
+    assert rep.strategy == P.strategy_label(strat)
+    pool = pool_from_golden(g)
+    for k in range(int(g["steps"])):
+        assert P.step(pool, cfg, k).force_evals == int(g["s%d_evals" % k])
+    assert pool.state_hash() == str(g["state_hash"])
+
+
 def test_build_grid_matches_oracle(cuda_required):
     import paper_2105_00039_b200 as P
     g = load_golden("rand600_s1_f64")
