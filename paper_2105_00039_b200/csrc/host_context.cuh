@@ -105,6 +105,7 @@ struct cg_context {
     int64_t lvl_epoch[3] = {-1, -1, -1};     // list_builds when written
     double lvl_D[3] = {}, lvl_delta[3] = {};
     int lvl_parent[3] = {};
+    bool sub_built = false;   // the last list build also wrote both sub-lists (run_sweep)
     int64_t inner_steps = 0;      // list steps that swept a sub-list
     int64_t nbr_cap = 0;
     int nbr_width = 0;            // entries per agent allocated

@@ -3,6 +3,11 @@
 // Included once, in order, by cellgrid_b200.cu; not a standalone header.
 #pragma once
 
+// 1: a sparse list build also writes the middle and short sub-lists (run_sweep)
+#ifndef CG_BUILD_SUBLISTS
+#define CG_BUILD_SUBLISTS 1
+#endif
+
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
 // idx (or, when relayout, the records in slot order in the alternate buffers).
 static int ensure_big(cg_context *c);
@@ -315,7 +320,8 @@ static void bbox_shell(const cg_context *c, double md, double shell_lo[3], doubl
 }
 
 template <typename T>
-static int run_sweep(cg_context *c, const double params[5], bool freeze, bool record, bool build_lists = false)
+static int run_sweep(cg_context *c, const double params[5], bool freeze, bool record, bool build_lists = false,
+                     bool subs = false)
 {
     const int n = (int)c->n;
     cudaStream_t st = c->stream;
@@ -400,6 +406,26 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
         A.list_cap = c->list_width;
         A.skin = (T)c->list_skin_used;
         A.skin_f = nextafterf((float)c->list_skin_used, INFINITY);
+    }
+    // the two sub-lists written with the list (single context, the sweep7
+    // list builds; the dense warp build writes only the list)
+    c->sub_built = false;
+    if (build_lists && subs && CG_BUILD_SUBLISTS && c->lvl_nbr[1] && c->lvl_nbr[2] && c->lvl_frac[1] > 0.0 &&
+        c->lvl_frac[2] > 0.0 && c->lvl_frac[2] < c->lvl_frac[1] && c->lvl_frac[1] < 1.0 &&
+        (!c->last_dense || 4.19 * (double)n / (double)c->geo.nb <= 20.0)) {
+        A.sub1 = c->lvl_nbr[1];
+        A.sub1_n = c->lvl_n[1];
+        A.sub2 = c->lvl_nbr[2];
+        A.sub2_n = c->lvl_n[2];
+        A.sub1_d = (T)(c->lvl_frac[1] * c->list_skin_used);
+        A.sub2_d = (T)(c->lvl_frac[2] * c->list_skin_used);
+        if (sizeof(T) == 8 && c->min_diam == c->max_diam && std::isfinite(c->max_diam)) {
+            const T ri = (T)c->max_diam * T(0.5);
+            const T rsum = ri + ri;
+            A.u_sub1 = rsum + A.sub1_d;
+            A.u_sub2 = rsum + A.sub2_d;
+        }
+        c->sub_built = true;
     }
     int rc = launch_sweep7<T>(c, A);
     if (rc) return rc;
@@ -832,10 +858,19 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
         }
         if (c->early.want && (rc = early_download<T>(c))) return rc;
         c->list_valid = false;
-        if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
+        if ((rc = run_sweep<T>(c, params, freeze, record, build, true))) return rc;
         c->last_kind = build ? 1 : 0;
         S.sweep_kind = build ? 1 : 0;
         if (build) c->list_builds++;
+        if (build && c->sub_built) {   // both sub-lists hold the build's partners within their delta
+            for (int k = 1; k <= 2; ++k) {
+                c->lvl_delta[k] = c->lvl_frac[k] * c->list_skin_used;
+                c->lvl_valid[k] = true;
+                c->lvl_written[k] = true;
+                c->lvl_epoch[k] = c->list_builds;
+                c->lvl_parent[k] = k - 1;
+            }
+        }
     }
     c->last_freeze = freeze;
     if (!freeze) c->cur_pos = 1 - c->cur_pos;

@@ -81,6 +81,11 @@ struct Sweep7Args {
     // UNI (every diameter equal, fp64): the pair constants in the kernel's
     // expression order -- rsum = ri + ri, req = (ri * ri) / rsum, lim = rsum + skin
     T u_rsum, u_req, u_lim;
+    // LIST: the two sub-lists (partners within ri + rj + sub1_d / sub2_d,
+    // sub2_d < sub1_d < skin, list order) written with the list, so the list
+    // steps after a build sweep the short sub-list at once; nullptr: not written
+    int *sub1, *sub1_n, *sub2, *sub2_n;
+    T sub1_d, sub2_d, u_sub1, u_sub2;   // u_*: UNI, rsum + sub*_d
 };
 
 constexpr int kListCap = 48;    // list width of sparse pools (dense pools: sized from the density)
@@ -262,7 +267,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         const T xi = me.x, yi = me.y, zi = me.z;
         const T ri = me.d * half;
         T fx = zero, fy = zero, fz = zero;
-        int nk = 0, nd = 0, nl = 0;
+        int nk = 0, nd = 0, nl = 0, n1 = 0, n2 = 0;
         T last_rj = T(-1), last_req = zero;
         // NOCALL (the main kernel when an overflow kernel follows): call-free
         // sqrt / division (common.cuh); an operand outside their fast range,
@@ -301,7 +306,17 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
 #endif
                 const T rsum = UNI ? A.u_rsum : ri + rj;
                 if (LIST && dist <= (UNI ? A.u_lim : rsum + A.skin)) {
-                    if (nl < A.list_cap) A.nbr[nl * A.nbr_stride + a] = jc;
+                    if (nl < A.list_cap) {
+                        A.nbr[nl * A.nbr_stride + a] = jc;
+                        if (A.sub1 && dist <= (UNI ? A.u_sub1 : rsum + A.sub1_d)) {
+                            A.sub1[n1 * A.nbr_stride + a] = jc;
+                            ++n1;
+                            if (dist <= (UNI ? A.u_sub2 : rsum + A.sub2_d)) {
+                                A.sub2[n2 * A.nbr_stride + a] = jc;
+                                ++n2;
+                            }
+                        }
+                    }
                     ++nl;
                 }
                 const T delta = rsum - dist;
@@ -491,6 +506,10 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
         A.disp_z[a] = ddz;
         if (LIST) {
             A.nbr_n[a] = nl;
+            if (A.sub1) {
+                A.sub1_n[a] = n1;
+                A.sub2_n[a] = n2;
+            }
             if (nl > A.list_cap) atomicAdd(A.slots + (blockIdx.x % kSlots) * kSlotWords + 10, 1ull);
         }
         if (LIST || ZSORTED)   // the step's largest displacement (list validity / build decision)
