@@ -486,7 +486,7 @@ static int slab_list_step(cg_context *c, const double params[5], bool freeze, bo
         c->launches += 1;
     }
     if (fused) {
-        const int gb = std::min(cdiv(g.nb, kThreads), c->sms * 8);
+        const int gb = std::min(cdiv(g.nb, kThreads), c->sms * CG_BOX_GRID);
         box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);
         box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->count_own, c->offset, c->slots, stat);
         LAUNCH_CHECK(c);

@@ -7,6 +7,12 @@
 #ifndef CG_BUILD_SUBLISTS
 #define CG_BUILD_SUBLISTS 1
 #endif
+// blocks per SM of the 27-box statistics passes of a list step (with the
+// block-level reduction of box_stencil_pass: 8 -> 16 measured 1.0087 -> 1.0016 ms
+// per list step, profiles/r2/ab_boxred.jsonl; 32 without it: +3 %)
+#ifndef CG_BOX_GRID
+#define CG_BOX_GRID 16
+#endif
 
 // Grid rebuild on the current storage.  Leaves key_rank, offset, skey, prox and
 // idx (or, when relayout, the records in slot order in the alternate buffers).
@@ -678,7 +684,7 @@ static int list_step_t(cg_context *c, const Geometry &g, const double params[5],
     bbox_shell(c, (double)A.p.max_disp, A.shell_lo, A.shell_hi);
     if (fused) {
         launch_list_sweep<T>(c, A, n, true, st);
-        const int gb = std::min(cdiv(g.nb, kThreads), c->sms * 8);
+        const int gb = std::min(cdiv(g.nb, kThreads), c->sms * CG_BOX_GRID);
         box_sum_yz<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, c->offset);   // offsets are unused on a fused step
         box_stencil_pass<<<gb, kThreads, 0, st>>>(g, c->bd, c->count, nullptr, c->offset, c->slots, stat);
         c->launches += 3;

@@ -412,6 +412,9 @@ __global__ void __launch_bounds__(kThreads) box_sum_yz(Geometry g, BoxDecode bd,
     }
 }
 
+#ifndef CG_BOX_BLOCK_REDUCE
+#define CG_BOX_BLOCK_REDUCE 1
+#endif
 __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDecode bd, int *__restrict__ count,
                                                              int *__restrict__ ghosts, const int *__restrict__ syz,
                                                              unsigned long long *__restrict__ slots,
@@ -443,11 +446,34 @@ __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDeco
     occ = warp_sum(occ);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+#if CG_BOX_BLOCK_REDUCE
+    // one set of atomics per block: the occupancy words are two addresses
+    // every block hits (same-address atomics serialise in L2)
+    __shared__ unsigned long long red[3][kThreads / 32];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = cand;
+        red[1][w] = occ;
+        red[2][w] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kThreads / 32; ++k) {
+            cand += red[0][k];
+            occ += red[1][k];
+            mx = max(mx, red[2][k]);
+        }
+        if (cand) atomicAdd(slots + (blockIdx.x % kSlots) * kSlotWords + 7, cand);
+        if (occ) atomicAdd(stat + 0, occ);
+        if (mx) atomicMax(stat + 1, mx);
+    }
+#else
     if ((threadIdx.x & 31) == 0) {
         if (cand) atomicAdd(slots + (blockIdx.x % kSlots) * kSlotWords + 7, cand);
         if (occ) atomicAdd(stat + 0, occ);
         if (mx) atomicMax(stat + 1, mx);
     }
+#endif
 }
 
 // slab list steps: the ghosts' boxes join the counts (owned agents are
