@@ -3,10 +3,6 @@
 // Included once, in order, by cellgrid_b200.cu; not a standalone header.
 #pragma once
 
-// 1: a sparse list build also writes the middle and short sub-lists (run_sweep)
-#ifndef CG_BUILD_SUBLISTS
-#define CG_BUILD_SUBLISTS 1
-#endif
 // blocks per SM of the 27-box statistics passes of a list step (with the
 // block-level reduction of box_stencil_pass: 8 -> 16 measured 1.0087 -> 1.0016 ms
 // per list step, profiles/r2/ab_boxred.jsonl; 32 without it: +3 %)
@@ -416,7 +412,7 @@ static int run_sweep(cg_context *c, const double params[5], bool freeze, bool re
     // the two sub-lists written with the list (single context, the sweep7
     // list builds; the dense warp build writes only the list)
     c->sub_built = false;
-    if (build_lists && subs && CG_BUILD_SUBLISTS && c->lvl_nbr[1] && c->lvl_nbr[2] && c->lvl_frac[1] > 0.0 &&
+    if (build_lists && subs && c->lvl_nbr[1] && c->lvl_nbr[2] && c->lvl_frac[1] > 0.0 &&
         c->lvl_frac[2] > 0.0 && c->lvl_frac[2] < c->lvl_frac[1] && c->lvl_frac[1] < 1.0 &&
         (!c->last_dense || 4.19 * (double)n / (double)c->geo.nb <= 20.0)) {
         A.sub1 = c->lvl_nbr[1];

@@ -299,12 +299,8 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
                 }
             }
             if (s2 > (UNI ? A.u_bound : rsum * rsum * kfac)) continue;
-#if CG_SEEDED_DIV
             T rs;
             const T dist = tsqrt_nocall_r(s2, ok, rs);
-#else
-            const T dist = tsqrt_nocall(s2, ok);
-#endif
             const T delta = rsum - dist;
             if (!(delta > zero)) continue;
             ++nk;
@@ -315,11 +311,7 @@ __global__ void __launch_bounds__(kListThreads, CG_LIST_MINB) list_sweep_kernel(
                 last_req = tdiv_nocall(ri * rj, rsum, ok);
             }
             const T mag = A.p.kappa * delta - A.p.gamma * tsqrt_nocall(last_req * delta, ok);
-#if CG_SEEDED_DIV
             const T sc = tdiv_seeded(mag, dist, rs, ok);   // dist == 0 (coincident centres): not ok
-#else
-            const T sc = tdiv_nocall(mag, dist, ok);   // dist == 0 (coincident centres): not ok
-#endif
             fx = fx + sc * dx;
             fy = fy + sc * dy;
             fz = fz + sc * dz;
@@ -412,9 +404,6 @@ __global__ void __launch_bounds__(kThreads) box_sum_yz(Geometry g, BoxDecode bd,
     }
 }
 
-#ifndef CG_BOX_BLOCK_REDUCE
-#define CG_BOX_BLOCK_REDUCE 1
-#endif
 __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDecode bd, int *__restrict__ count,
                                                              int *__restrict__ ghosts, const int *__restrict__ syz,
                                                              unsigned long long *__restrict__ slots,
@@ -446,7 +435,6 @@ __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDeco
     occ = warp_sum(occ);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-#if CG_BOX_BLOCK_REDUCE
     // one set of atomics per block: the occupancy words are two addresses
     // every block hits (same-address atomics serialise in L2)
     __shared__ unsigned long long red[3][kThreads / 32];
@@ -467,13 +455,6 @@ __global__ void __launch_bounds__(kThreads) box_stencil_pass(Geometry g, BoxDeco
         if (occ) atomicAdd(stat + 0, occ);
         if (mx) atomicMax(stat + 1, mx);
     }
-#else
-    if ((threadIdx.x & 31) == 0) {
-        if (cand) atomicAdd(slots + (blockIdx.x % kSlots) * kSlotWords + 7, cand);
-        if (occ) atomicAdd(stat + 0, occ);
-        if (mx) atomicMax(stat + 1, mx);
-    }
-#endif
 }
 
 // slab list steps: the ghosts' boxes join the counts (owned agents are

@@ -297,13 +297,9 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 }
                 const T dx = xi - co.x, dy = yi - co.y, dz = zi - co.z;   // kernels.py:198-203
                 const T rj = UNI ? zero : co.d * half;
-#if CG_SEEDED_DIV
                 T rs = zero;   // NOCALL: dist's rsqrt estimate seeds the division by dist
                 const T dist = NOCALL ? tsqrt_nocall_r(dx * dx + dy * dy + dz * dz, ok, rs)
                                       : tsqrt<T>(dx * dx + dy * dy + dz * dz);
-#else
-                const T dist = xsqrt(dx * dx + dy * dy + dz * dz);
-#endif
                 const T rsum = UNI ? A.u_rsum : ri + rj;
                 if (LIST && dist <= (UNI ? A.u_lim : rsum + A.skin)) {
                     if (nl < A.list_cap) {
@@ -330,11 +326,7 @@ __device__ __forceinline__ void sweep_agent(const Sweep7Args<T> &A, const int s,
                 }
                 const T mag = A.p.kappa * delta - A.p.gamma * xsqrt(last_req * delta);
                 if (NOCALL || dist > zero) {   // NOCALL: dist == 0 fails the division's range test
-#if CG_SEEDED_DIV
                     const T sc = NOCALL ? tdiv_seeded(mag, dist, rs, ok) : mag / dist;
-#else
-                    const T sc = xdiv(mag, dist);
-#endif
                     fx = fx + sc * dx;
                     fy = fy + sc * dy;
                     fz = fz + sc * dz;
