@@ -356,3 +356,35 @@ def test_coincident_centres_on_list_steps(cuda_required, fp32):
         assert a[0] == b[0], k
         for col in a[1]:
             assert np.array_equal(a[1][col], b[1][col]), (k, col)
+
+
+def test_build_writes_the_sub_lists(cuda_required):
+    """A sparse list build also writes the middle and short sub-lists
+    (host_step.cuh run_sweep, sweep7.cuh LIST): every list step after the
+    build sweeps a sub-list -- none refreshes from the whole list while the
+    motion stays inside the short list's delta -- and the steps equal the C
+    oracle bit for bit."""
+    from paper_2105_00039_b200 import _native as N
+    from paper_2105_00039_b200.mechanics import ForceParams
+    pool = POOLS[0][1]
+    ref = pool.copy()
+    ctx = N.Context(0, pool.dtype)
+    ctx.set_option(N.CG_OPT_SUMMATION, 0)
+    ctx.set_option(N.CG_OPT_LIST_SKIN, -1)
+    ctx.upload(pool.position_x, pool.position_y, pool.position_z, pool.diameter, pool.adherence, pool.uid)
+    kinds = []
+    for k in range(4):
+        st = ctx.step(PARAMS5, None, 1 << 24, N.CG_STEP_SORT)
+        kinds.append(int(st.sweep_kind))
+        r = oracle.step(ref, ForceParams(), sort=True, threads=8)
+        assert (st.force_evals, st.candidates, st.degenerate_pairs) == (
+            r.force_evals, r.candidates, r.degenerate_pairs), k
+        cols = ctx.download()
+        for a, b in (("px", "position_x"), ("dx", "displacement_x"), ("dz", "displacement_z")):
+            assert np.array_equal(cols[a], getattr(ref, b)), (k, a)
+    stats = ctx.list_stats()
+    ctx.close()
+    assert kinds[:2] == [0, 1] and kinds[2] == 2, kinds
+    # the first list step right after the build already swept a sub-list
+    n_list = kinds.count(2)
+    assert stats["list_steps"] == n_list and stats["inner_steps"] == n_list, (kinds, stats)
