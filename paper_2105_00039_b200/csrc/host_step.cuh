@@ -6,6 +6,18 @@
 // blocks per SM of the 27-box statistics passes of a list step (with the
 // block-level reduction of box_stencil_pass: 8 -> 16 measured 1.0087 -> 1.0016 ms
 // per list step, profiles/r2/ab_boxred.jsonl; 32 without it: +3 %)
+// dense moving pools: a build (C2: 2.7 ms) pays off over a grid sweep
+// (0.72 ms) only if its lists serve ~4 steps (0.23 ms each): no build while
+// the last step's largest displacement exceeds skin / 12 (expected life < 6),
+// and lists that served fewer than 5 steps back the next builds off
+// (C2 over 100 steps 0.84 -> 0.67 ms, moving C3-27 1.64 -> 1.32 ms,
+// profiles/r2/ab_dense.jsonl)
+#ifndef CG_DENSE_LIFE
+#define CG_DENSE_LIFE 12.0
+#endif
+#ifndef CG_DENSE_MIN_LIFE
+#define CG_DENSE_MIN_LIFE 5
+#endif
 #ifndef CG_BOX_GRID
 #define CG_BOX_GRID 16
 #endif
@@ -819,7 +831,7 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
             use_list = true;
         } else {   // expired: a list that served fewer than 2 steps makes the next builds wait
             c->list_valid = false;
-            if (c->list_life < 2) {
+            if (c->list_life < (c->list_width != kListCap ? CG_DENSE_MIN_LIFE : 2)) {
                 c->list_backoff = c->list_backoff ? std::min(2 * c->list_backoff, 64) : 4;
                 c->list_wait = c->list_backoff;
             } else {
@@ -844,9 +856,10 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
             c->list_width = build ? list_width_for(c, g, c->list_skin_used) : 0;
             build = build && c->list_width > 0;
             // dense pools: no build while the last moving step moved some agent by
-            // more than skin / 4 (the lists would not serve 2 steps)
+            // more than skin / CG_DENSE_LIFE (the lists would not serve
+            // CG_DENSE_LIFE / 2 steps)
             if (build && c->list_width != kListCap && !freeze && !c->last_freeze &&
-                4.0 * std::sqrt(std::max(c->bbox_host[7], 0.0)) > c->list_skin_used)
+                CG_DENSE_LIFE * std::sqrt(std::max(c->bbox_host[7], 0.0)) > c->list_skin_used)
                 build = false;
             if (build && (rc = ensure_lists(c, c->list_width))) return rc;
         }
