@@ -239,8 +239,8 @@ static int launch_sweep7(cg_context *c, const Sweep7Args<T> &A)
                     <<<g1, kThreads, 0, st>>>(A);
                 sweep7_overflow<T, true, false, CG_LIST_BUILD_KS, true, true><<<g2, kThreads, 0, st>>>(A);
             } else if (A.uid32) {
-                sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true, true><<<g1, kThreads, 0, st>>>(A);
-                sweep7_overflow<T, true, false, 16, true, true><<<g2, kThreads, 0, st>>>(A);
+                sweep7_kernel<T, true, false, CG_LIST_BUILD_KS, false, CG_LIST_BUILD_MINB, true, true><<<g1, kThreads, 0, st>>>(A);
+                sweep7_overflow<T, true, false, CG_LIST_BUILD_KS, true, true><<<g2, kThreads, 0, st>>>(A);
             } else {
                 sweep7_kernel<T, true, false, 16, false, CG_LIST_BUILD_MINB, true><<<g1, kThreads, 0, st>>>(A);
                 sweep7_overflow<T, true, false, 16, true><<<g2, kThreads, 0, st>>>(A);
