@@ -555,10 +555,11 @@ static int slab_step_t(cg_context *c, const double params[5], int flags, int64_t
                 c->list_skin_used = c->list_skin < 0 ? 0.26 * S.g.L : c->list_skin;   // slab lists are 48 wide
                 build = c->list_skin_used > 0 && c->list_skin_used <= S.g.L;
             }
-            if ((rc = run_sweep<T>(c, params, freeze, record, build))) return rc;
+            if ((rc = run_sweep<T>(c, params, freeze, record, build, true))) return rc;
             if (build) {
                 if ((rc = slab_list_tables<T>(c))) return rc;
                 c->list_builds++;
+                mark_build_sublists(c);
             }
             if (!freeze) c->cur_pos = 1 - c->cur_pos;
         } else {

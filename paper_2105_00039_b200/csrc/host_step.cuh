@@ -333,6 +333,20 @@ static void bbox_shell(const cg_context *c, double md, double shell_lo[3], doubl
     }
 }
 
+// After a list build (list_builds already counted): if the build also wrote
+// both sub-lists (run_sweep), they hold its partners within their deltas
+static void mark_build_sublists(cg_context *c)
+{
+    if (!c->sub_built) return;
+    for (int k = 1; k <= 2; ++k) {
+        c->lvl_delta[k] = c->lvl_frac[k] * c->list_skin_used;
+        c->lvl_valid[k] = true;
+        c->lvl_written[k] = true;
+        c->lvl_epoch[k] = c->list_builds;
+        c->lvl_parent[k] = k - 1;
+    }
+}
+
 template <typename T>
 static int run_sweep(cg_context *c, const double params[5], bool freeze, bool record, bool build_lists = false,
                      bool subs = false)
@@ -877,15 +891,7 @@ static int step_impl(cg_context *c, const double params[5], double ir, int64_t b
         c->last_kind = build ? 1 : 0;
         S.sweep_kind = build ? 1 : 0;
         if (build) c->list_builds++;
-        if (build && c->sub_built) {   // both sub-lists hold the build's partners within their delta
-            for (int k = 1; k <= 2; ++k) {
-                c->lvl_delta[k] = c->lvl_frac[k] * c->list_skin_used;
-                c->lvl_valid[k] = true;
-                c->lvl_written[k] = true;
-                c->lvl_epoch[k] = c->list_builds;
-                c->lvl_parent[k] = k - 1;
-            }
-        }
+        if (build) mark_build_sublists(c);
     }
     c->last_freeze = freeze;
     if (!freeze) c->cur_pos = 1 - c->cur_pos;
