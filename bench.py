@@ -416,6 +416,7 @@ def main_slab(args, rank, world, local):
 
 EXTRAS = (   # (key, config, precision, summation, list skin, sort_every, freeze) -- BASELINE.json configs
     ("c4_lists_off", "c4", "fp64", "uid", 0, 1, False),     # the literal "grid rebuild each step"
+    ("c1_fp64", "c1", "fp64", "uid", -1, 1, False),         # the reference's own CPU-runnable case (32^3)
     ("c2_fp64", "c2", "fp64", "uid", -1, 1, False),
     ("c2_fp32", "c2", "fp32", "uid", -1, 1, False),
     ("c3_4_sorted", "c3_4", "fp64", "uid", -1, 1, True),
